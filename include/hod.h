@@ -1,0 +1,138 @@
+/*
+ * hod.h — C ABI of the Holmes Overlapped Distributed-optimizer (HOD) data path
+ * on B200 (sm_100a).
+ *
+ * The reference (arXiv 2312.03549, /root/reference/pkg) has NO native optimizer:
+ * it only PRICES the data-parallel gradient synchronisation of a pipeline stage
+ * as reduce-scatter + all-gather of the stage's gradient bytes
+ *   - CostModel.reduce_scatter / CostModel.all_gather   simulator.py:81-89
+ *   - dp_sync per stage (max over the stage's DP rows)  simulator.py:327-333
+ *   - post-flush placement                              simulator.py:445-452
+ *   - gradient-set size                                 simulator.py:268-280
+ * and imports the real optimizer from Megatron-LM / Megatron-LLaMA.
+ * Every entry point below is the device-side operation behind one of those
+ * priced terms.  A host binding (ctypes, cgo,
+ * JNI, ...) needs nothing but this header: plain pointers, sizes, and a
+ * cudaStream_t passed as void*.
+ *
+ * Conventions
+ *   - return 0 on success; a non-zero value is a cudaError_t / ncclResult_t /
+ *     HOD_E* code and hod_last_error() returns a thread-local message.
+ *   - every buffer is caller-owned device memory (allocated by PyTorch); the
+ *     library never allocates persistent device memory (NCCL's internal
+ *     buffers excepted) and never synchronises the host inside a step.
+ *   - "bf16" buffers are uint16_t bit patterns; rounding is IEEE RNE.
+ *   - all kernels are compiled for sm_100a only; there is no CPU fallback.
+ */
+#ifndef HOD_H_
+#define HOD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HOD_ABI_VERSION 1
+
+/* library-level error codes (outside the cudaError_t / ncclResult_t ranges) */
+#define HOD_OK 0
+#define HOD_EINVAL 10001   /* bad argument (null pointer, negative size, ...) */
+#define HOD_EALIGN 10002   /* a buffer violates the documented alignment     */
+#define HOD_ETIMEOUT 10003 /* a cross-GPU wait exceeded its spin budget      */
+#define HOD_ENCCL 10004    /* NCCL returned an error (message has details)   */
+
+/* source dtype of a gradient tensor fed to the packer */
+#define HOD_DTYPE_BF16 0
+#define HOD_DTYPE_F32 1
+
+/* maximum tensors in one hod_pack_bf16 call (larger tables are split) */
+#define HOD_PACK_MAX_ENTRIES 64
+
+/* number of per-bucket partial sums written by hod_sumsq_bf16 */
+#define HOD_SUMSQ_PARTIALS 296
+
+/* One gradient tensor of a bucket: `numel` elements of `src` (dtype given to
+ * the call) land at bucket[dst_offset .. dst_offset+numel).  Entries must be
+ * sorted by dst_offset and must not overlap; elements of the bucket covered
+ * by no entry (alignment gaps, tail padding) are written as +0.0. */
+typedef struct hod_pack_entry {
+  const void* src;
+  int64_t numel;
+  int64_t dst_offset;
+} hod_pack_entry;
+
+/* AdamW hyper-parameters for one step.  The library folds them into fp32
+ * constants exactly as documented in DESIGN.md §K2 (decoupled weight decay,
+ * torch.optim.AdamW algebra). */
+typedef struct hod_adamw_params {
+  double lr;
+  double beta1;
+  double beta2;
+  double eps;
+  double weight_decay;
+  int64_t step; /* 1-based step count used for bias correction */
+} hod_adamw_params;
+
+/* ---- version / errors ---------------------------------------------------- */
+int hod_abi_version(void);
+const char* hod_last_error(void);
+
+/* ---- K1: bucket pack + dp-scale + bf16 cast ---------------
+ * bucket[dst_offset + i] = bf16_rne(float(src[i]) * scale), zeros elsewhere.
+ * `entries` is a HOST array (copied into the kernel's parameter space).
+ * Replaces the reference's implicit "gradient bytes of a stage"
+ * (simulator.py:268-280) with the actual flattened bucket. */
+int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket,
+                  int64_t bucket_numel, float scale, int src_dtype, void* stream);
+
+/* ---- K3: deterministic sum of squares of a bf16 shard -----
+ * Writes HOD_SUMSQ_PARTIALS fp32 partial sums to partials[0..HOD_SUMSQ_PARTIALS)
+ * (fixed grid, fixed order => bit-reproducible for a given n). */
+int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream);
+
+/* Sums `n_partials` fp32 partials in fixed order (fp64 accumulator) and writes
+ * the fp32 result to *out. */
+int hod_sum_partials(const float* partials, int64_t n_partials, float* out,
+                     void* stream);
+
+/* coef = min(1, max_norm / (sqrt(*sumsq) + 1e-6)); *norm = sqrt(*sumsq).
+ * torch.nn.utils.clip_grad_norm_ convention. */
+int hod_clip_coef(const float* sumsq, float max_norm, float* coef, float* norm,
+                  void* stream);
+
+/* ---- K2: fused sharded AdamW ------------------------------
+ * For i in [0,n): g = float(grad[i]) (* *clip_coef if clip_coef != NULL);
+ * master/m/v updated in place; param[i] = bf16_rne(master[i]).
+ * 28 bytes of HBM traffic per element.  clip_coef is a DEVICE pointer. */
+int hod_adamw_bf16(float* master, float* exp_avg, float* exp_avg_sq,
+                   const uint16_t* grad, uint16_t* param, int64_t n,
+                   const hod_adamw_params* hp, const float* clip_coef, void* stream);
+
+/* Same update reading an fp32 gradient (fp32 reduce-scatter parity mode). */
+int hod_adamw_f32(float* master, float* exp_avg, float* exp_avg_sq,
+                  const float* grad, uint16_t* param, int64_t n,
+                  const hod_adamw_params* hp, const float* clip_coef, void* stream);
+
+/* ---- C1-C3: NCCL collectives over NVLink (§8e) ---------
+ * Communicators are built from GroupPlan DP rows (groups.py:137-148), ranks
+ * converted 1-based -> 0-based by the host. */
+int hod_nccl_unique_id(uint8_t out[128]);
+int hod_nccl_comm_init(const uint8_t id[128], int nranks, int rank, void** comm);
+int hod_comm_destroy(void* comm);
+/* sum-reduce-scatter: recv (recvcount bf16) = sum over ranks of
+ * send[rank*recvcount .. (rank+1)*recvcount).  In-place allowed when
+ * recv == send + rank*recvcount. (prices: simulator.py:81-84) */
+int hod_reduce_scatter_bf16(const void* send, void* recv, size_t recvcount, void* comm,
+                            void* stream);
+/* all-gather: recv[r*sendcount ..] = rank r's send.  In-place allowed when
+ * send == recv + rank*sendcount. (prices: simulator.py:86-89) */
+int hod_all_gather_bf16(const void* send, void* recv, size_t sendcount, void* comm,
+                        void* stream);
+int hod_all_reduce_f32(float* buf, size_t n, void* comm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOD_H_ */

@@ -1,0 +1,97 @@
+"""ctypes binding of the in-tree sm_100a library ``libhod.so`` (include/hod.h).
+
+This is the only door from Python to the device data path.  There is no
+fallback: if the library is missing or cannot be loaded the import of any
+compute entry point raises, loudly, instead of silently running something
+else on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from pathlib import Path
+
+from .errors import DeviceError
+
+LIB_PATH = Path(__file__).resolve().parent / "libhod.so"
+
+HOD_PACK_MAX_ENTRIES = 64
+HOD_SUMSQ_PARTIALS = 296
+HOD_DTYPE_BF16 = 0
+HOD_DTYPE_F32 = 1
+
+# every symbol include/hod.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "hod_abi_version", "hod_last_error",
+    "hod_pack_bf16", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
+    "hod_adamw_bf16", "hod_adamw_f32",
+    "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
+    "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
+)
+
+
+class PackEntry(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("numel", ctypes.c_int64), ("dst_offset", ctypes.c_int64)]
+
+
+class AdamWParams(ctypes.Structure):
+    _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("step", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def load(build_if_missing: bool = True):
+    """Load libhod.so (building it in-tree first if it is absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    import torch  # noqa: F401  (loads the pip libnccl.so.2 our library links to)
+
+    if not LIB_PATH.exists() and build_if_missing:
+        from .build_native import build
+
+        build()
+    if not LIB_PATH.exists():
+        raise DeviceError(f"CUDA library {LIB_PATH} is missing; run "
+                          "`python -m paper_2312_03549_b200.build_native`")
+    L = ctypes.CDLL(str(LIB_PATH))
+    P, I64, I, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
+    sig = {
+        "hod_abi_version": ([], I),
+        "hod_last_error": ([], ctypes.c_char_p),
+        "hod_pack_bf16": ([ctypes.POINTER(PackEntry), I, P, I64, F, I, P], I),
+        "hod_sumsq_bf16": ([P, I64, P, P], I),
+        "hod_sum_partials": ([P, I64, P, P], I),
+        "hod_clip_coef": ([P, F, P, P, P], I),
+        "hod_adamw_bf16": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
+        "hod_adamw_f32": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
+        "hod_nccl_unique_id": ([P], I),
+        "hod_nccl_comm_init": ([P, I, I, ctypes.POINTER(ctypes.c_void_p)], I),
+        "hod_comm_destroy": ([P], I),
+        "hod_reduce_scatter_bf16": ([P, P, ctypes.c_size_t, P, P], I),
+        "hod_all_gather_bf16": ([P, P, ctypes.c_size_t, P, P], I),
+        "hod_all_reduce_f32": ([P, ctypes.c_size_t, P, P], I),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        msg = load().hod_last_error().decode(errors="replace")
+        raise DeviceError(f"{what} failed (code {rc}): {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(load(), name)(*args), name)
+
+
+def stream_ptr(stream) -> int:
+    """cudaStream_t handle of a torch.cuda.Stream (0 = legacy default)."""
+    return int(stream.cuda_stream) if stream is not None else 0

@@ -1,0 +1,87 @@
+// hod_common.cuh — shared helpers for the HOD sm_100a kernels.
+//
+// Arithmetic here is written with explicit-rounding intrinsics (__fmul_rn,
+// __fadd_rn, __fdiv_rn, __fsqrt_rn) so that nvcc cannot contract into FMA:
+// the CPU oracle (oracle/hod_oracle.c, built with -ffp-contract=off) performs
+// the identical IEEE operations in the identical order, which makes the
+// device results bit-exact against it.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hod.h"
+
+namespace hod {
+
+// Thread-local error slot behind hod_last_error().
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+constexpr int kThreads = 256;
+constexpr int kSMs = 148;
+
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) {
+  return __uint_as_float(static_cast<uint32_t>(h) << 16);
+}
+
+// IEEE round-to-nearest-even fp32 -> bf16 (NaN stays NaN, quieted).
+__device__ __forceinline__ uint16_t f32_to_bf16(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x0040u);
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+// Unpack 8 bf16 from a uint4 into floats.
+__device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    w[i] = static_cast<uint32_t>(f32_to_bf16(f[2 * i])) |
+           (static_cast<uint32_t>(f32_to_bf16(f[2 * i + 1])) << 16);
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// Fp32 AdamW constants folded on the host in double precision, then rounded
+// once to fp32.
+struct AdamWConsts {
+  float decay;      // 1 - lr*wd
+  float b1, omb1;   // beta1, 1-beta1
+  float b2, omb2;   // beta2, 1-beta2
+  float step_size;  // lr / (1 - beta1^t)
+  float bc2_sqrt;   // sqrt(1 - beta2^t)
+  float eps;
+};
+
+AdamWConsts fold_adamw(const hod_adamw_params& hp);
+
+// One element of the update; identical op order to oracle/hod_oracle.c.
+__device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g,
+                                           const AdamWConsts& c) {
+  p = __fmul_rn(p, c.decay);
+  m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, g));
+  v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.omb2, __fmul_rn(g, g)));
+  const float den = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.bc2_sqrt), c.eps);
+  p = __fsub_rn(p, __fmul_rn(c.step_size, __fdiv_rn(m, den)));
+}
+
+inline int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 8) {
+  int64_t need = (work_items + per_block - 1) / per_block;
+  int64_t cap = static_cast<int64_t>(kSMs) * max_blocks_per_sm;
+  if (need < 1) need = 1;
+  return static_cast<int>(need < cap ? need : cap);
+}
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace hod

@@ -1,0 +1,376 @@
+// hod_kernels.cu — K1 (bucket pack/cast), K2 (fused sharded AdamW) and K3
+// (deterministic grad sum-of-squares + clip coefficient) for sm_100a.
+//
+// All three are elementwise and HBM-bound: no tensor
+// cores, 128-bit coalesced loads/stores, grid sized in multiples of the 148
+// SMs and grid-strided.  See include/hod.h for the contracts.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "hod_common.cuh"
+
+namespace hod {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return HOD_OK;
+  set_error("%s: %s (%d)", what, cudaGetErrorString(e), static_cast<int>(e));
+  return static_cast<int>(e);
+}
+
+AdamWConsts fold_adamw(const hod_adamw_params& hp) {
+  AdamWConsts c;
+  const double t = static_cast<double>(hp.step);
+  const double bc1 = 1.0 - pow(hp.beta1, t);
+  const double bc2 = 1.0 - pow(hp.beta2, t);
+  c.decay = static_cast<float>(1.0 - hp.lr * hp.weight_decay);
+  c.b1 = static_cast<float>(hp.beta1);
+  c.omb1 = static_cast<float>(1.0 - hp.beta1);
+  c.b2 = static_cast<float>(hp.beta2);
+  c.omb2 = static_cast<float>(1.0 - hp.beta2);
+  c.step_size = static_cast<float>(hp.lr / bc1);
+  c.bc2_sqrt = static_cast<float>(sqrt(bc2));
+  c.eps = static_cast<float>(hp.eps);
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// K1: pack.  The table travels by value in the kernel parameter space
+// (constant bank), so a CTA-uniform scan over it is a broadcast read.  Each
+// CTA owns tiles of kPackTile destination elements; a tile that lies inside
+// one tensor with a 16-byte-aligned source takes the vector path, the few
+// tiles touching a tensor boundary or padding take the scalar path.
+// ---------------------------------------------------------------------------
+constexpr int kPackVec = 8;                          // elements per 16-byte bf16 store
+constexpr int kPackUnroll = 4;
+constexpr int kPackTile = kThreads * kPackVec * kPackUnroll;  // 8192 elements
+
+struct PackTable {
+  const void* src[HOD_PACK_MAX_ENTRIES];
+  int64_t numel[HOD_PACK_MAX_ENTRIES];
+  int64_t off[HOD_PACK_MAX_ENTRIES];
+  uint64_t vec_ok;  // bit i: src[i] is 16-byte aligned
+  int n;
+};
+
+template <typename SrcT>
+__device__ __forceinline__ float load_src(const void* p, int64_t i) {
+  if constexpr (sizeof(SrcT) == 2)
+    return bf16_to_f32(static_cast<const uint16_t*>(p)[i]);
+  else
+    return static_cast<const float*>(p)[i];
+}
+
+template <typename SrcT>
+__device__ __forceinline__ void load8(const void* p, int64_t i, float (&f)[8]) {
+  if constexpr (sizeof(SrcT) == 2) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(p) + i));
+    unpack8(q, f);
+  } else {
+    const float4* s = reinterpret_cast<const float4*>(static_cast<const float*>(p) + i);
+    const float4 a = __ldg(s), b = __ldg(s + 1);
+    f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+    f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+  }
+}
+
+template <typename SrcT>
+__global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ PackTable t,
+                                                         uint16_t* __restrict__ dst,
+                                                         int64_t bucket_numel, float scale) {
+  const int64_t n_tiles = (bucket_numel + kPackTile - 1) / kPackTile;
+  int e = 0;  // entry cursor; tiles visited by a CTA are increasing
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t a = tile * kPackTile;
+    const int64_t b = min(a + kPackTile, bucket_numel);
+    while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;  // CTA-uniform
+    const bool inside = e < t.n && t.off[e] <= a && b <= t.off[e] + t.numel[e];
+    if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kPackTile) {
+      const int64_t s0 = a - t.off[e];
+      float f[kPackUnroll][8];
+#pragma unroll
+      for (int u = 0; u < kPackUnroll; ++u)
+        load8<SrcT>(t.src[e], s0 + (static_cast<int64_t>(u) * kThreads + threadIdx.x) * kPackVec, f[u]);
+#pragma unroll
+      for (int u = 0; u < kPackUnroll; ++u) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[u][k] = __fmul_rn(f[u][k], scale);
+        reinterpret_cast<uint4*>(dst + a)[static_cast<int64_t>(u) * kThreads + threadIdx.x] = pack8(f[u]);
+      }
+    } else {
+      // boundary / padding tile: element-wise with a per-thread entry cursor
+      int ei = e;
+      for (int64_t i = a + threadIdx.x; i < b; i += kThreads) {
+        while (ei < t.n && t.off[ei] + t.numel[ei] <= i) ++ei;
+        float x = 0.0f;
+        if (ei < t.n && t.off[ei] <= i) x = __fmul_rn(load_src<SrcT>(t.src[ei], i - t.off[ei]), scale);
+        dst[i] = (ei < t.n && t.off[ei] <= i) ? f32_to_bf16(x) : static_cast<uint16_t>(0);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: AdamW.  Eight elements per thread per iteration: one 16-byte load of
+// bf16 grad, two 16-byte loads each of master/m/v; stores mirror them plus a
+// 16-byte bf16 param store.  28 B/element algorithmic traffic.
+// ---------------------------------------------------------------------------
+template <typename GradT, bool kClip>
+__global__ void __launch_bounds__(kThreads) adamw_vec_kernel(
+    float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+    const GradT* __restrict__ g, uint16_t* __restrict__ out, int64_t n_vec,
+    const AdamWConsts c, const float* __restrict__ coef_ptr) {
+  const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t iv = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; iv < n_vec; iv += stride) {
+    float gf[8];
+    if constexpr (sizeof(GradT) == 2) {
+      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + iv), gf);
+    } else {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(g) + 2 * iv);
+      const float4 b = __ldg(reinterpret_cast<const float4*>(g) + 2 * iv + 1);
+      gf[0] = a.x; gf[1] = a.y; gf[2] = a.z; gf[3] = a.w;
+      gf[4] = b.x; gf[5] = b.y; gf[6] = b.z; gf[7] = b.w;
+    }
+    float4* p4 = reinterpret_cast<float4*>(p) + 2 * iv;
+    float4* m4 = reinterpret_cast<float4*>(m) + 2 * iv;
+    float4* v4 = reinterpret_cast<float4*>(v) + 2 * iv;
+    float4 pa = p4[0], pb = p4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+    float pf[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+    float mf[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+    float vf[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float gk = kClip ? __fmul_rn(gf[k], coef) : gf[k];
+      adamw_elem(pf[k], mf[k], vf[k], gk, c);
+    }
+    p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
+    p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
+    m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
+    m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
+    v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
+    v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
+    reinterpret_cast<uint4*>(out)[iv] = pack8(pf);
+  }
+}
+
+template <typename GradT, bool kClip>
+__global__ void __launch_bounds__(kThreads) adamw_scalar_kernel(
+    float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+    const GradT* __restrict__ g, uint16_t* __restrict__ out, int64_t begin, int64_t n,
+    const AdamWConsts c, const float* __restrict__ coef_ptr) {
+  const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t i = begin + static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    float gi;
+    if constexpr (sizeof(GradT) == 2) gi = bf16_to_f32(g[i]); else gi = g[i];
+    if (kClip) gi = __fmul_rn(gi, coef);
+    float pi = p[i], mi = m[i], vi = v[i];
+    adamw_elem(pi, mi, vi, gi, c);
+    p[i] = pi; m[i] = mi; v[i] = vi;
+    out[i] = f32_to_bf16(pi);
+  }
+}
+
+template <typename GradT>
+static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const GradT* grad,
+                        uint16_t* param, int64_t n, const hod_adamw_params* hp,
+                        const float* clip_coef, cudaStream_t s) {
+  if (n < 0 || !hp) { set_error("hod_adamw: bad n/hp"); return HOD_EINVAL; }
+  if (n == 0) return HOD_OK;
+  if (!master || !exp_avg || !exp_avg_sq || !grad || !param) {
+    set_error("hod_adamw: null buffer"); return HOD_EINVAL;
+  }
+  if (hp->step < 1) { set_error("hod_adamw: step must be >= 1"); return HOD_EINVAL; }
+  const AdamWConsts c = fold_adamw(*hp);
+  const bool vec = aligned16(master) && aligned16(exp_avg) && aligned16(exp_avg_sq) &&
+                   aligned16(grad) && aligned16(param);
+  int64_t done = 0;
+  if (vec) {
+    const int64_t n_vec = n / 8;
+    if (n_vec > 0) {
+      const int grid = grid_for(n_vec, kThreads);
+      if (clip_coef)
+        adamw_vec_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef);
+      else
+        adamw_vec_kernel<GradT, false><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, nullptr);
+    }
+    done = n_vec * 8;
+  }
+  if (done < n) {
+    const int grid = grid_for(n - done, kThreads);
+    if (clip_coef)
+      adamw_scalar_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, clip_coef);
+    else
+      adamw_scalar_kernel<GradT, false><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, nullptr);
+  }
+  return cuda_status(cudaGetLastError(), "hod_adamw launch");
+}
+
+// ---------------------------------------------------------------------------
+// K3: sum of squares with a FIXED grid of HOD_SUMSQ_PARTIALS CTAs so the
+// per-CTA partials (and their fixed-order final sum) are reproducible.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float block_sum(float x) {
+  __shared__ float warp_part[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = x;
+  __syncthreads();
+  float s = 0.0f;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) s += warp_part[w];
+  return s;  // valid on thread 0
+}
+
+__global__ void __launch_bounds__(kThreads) sumsq_kernel(const uint16_t* __restrict__ x, int64_t n,
+                                                          bool vec, float* __restrict__ partials) {
+  float acc = 0.0f;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  int64_t tail_begin = 0;
+  if (vec) {
+    const int64_t n_vec = n / 8;
+    for (int64_t iv = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; iv < n_vec; iv += stride) {
+      float f[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(x) + iv), f);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc = __fadd_rn(acc, __fmul_rn(f[k], f[k]));
+    }
+    tail_begin = n_vec * 8;
+  }
+  for (int64_t i = tail_begin + static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < n; i += stride) {
+    const float f = bf16_to_f32(x[i]);
+    acc = __fadd_rn(acc, __fmul_rn(f, f));
+  }
+  const float s = block_sum(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void sum_partials_kernel(const float* __restrict__ partials, int64_t n, float* out) {
+  // one warp; lane-strided fp64 accumulation then a fixed shuffle tree
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 32) acc += static_cast<double>(partials[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x == 0) *out = static_cast<float>(acc);
+}
+
+__global__ void clip_coef_kernel(const float* sumsq, float max_norm, float* coef, float* norm) {
+  const float nrm = __fsqrt_rn(*sumsq);
+  const float c = __fdiv_rn(max_norm, __fadd_rn(nrm, 1e-6f));
+  *coef = c < 1.0f ? c : 1.0f;
+  if (norm) *norm = nrm;
+}
+
+}  // namespace hod
+
+using namespace hod;
+
+extern "C" {
+
+int hod_abi_version(void) { return HOD_ABI_VERSION; }
+
+const char* hod_last_error(void) { return g_err; }
+
+int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket,
+                  int64_t bucket_numel, float scale, int src_dtype, void* stream) {
+  if (!bucket || bucket_numel < 0 || n_entries < 0 || (n_entries > 0 && !entries)) {
+    set_error("hod_pack_bf16: bad arguments"); return HOD_EINVAL;
+  }
+  if (src_dtype != HOD_DTYPE_BF16 && src_dtype != HOD_DTYPE_F32) {
+    set_error("hod_pack_bf16: unknown src_dtype %d", src_dtype); return HOD_EINVAL;
+  }
+  if (!aligned16(bucket)) { set_error("hod_pack_bf16: bucket not 16-byte aligned"); return HOD_EALIGN; }
+  if (bucket_numel == 0) return HOD_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // validate ordering / bounds once on the host
+  int64_t prev_end = 0;
+  for (int i = 0; i < n_entries; ++i) {
+    const hod_pack_entry& e = entries[i];
+    if (!e.src || e.numel < 0 || e.dst_offset < prev_end || e.dst_offset + e.numel > bucket_numel) {
+      set_error("hod_pack_bf16: entry %d out of order or out of bounds", i); return HOD_EINVAL;
+    }
+    prev_end = e.dst_offset + e.numel;
+  }
+  // Split long tables into windows of HOD_PACK_MAX_ENTRIES; each launch covers
+  // the destination range [lo, hi) between its first and the next window.
+  int first = 0;
+  do {
+    const int cnt = (n_entries - first) < HOD_PACK_MAX_ENTRIES ? (n_entries - first) : HOD_PACK_MAX_ENTRIES;
+    const int64_t lo = (first == 0) ? 0 : entries[first].dst_offset;
+    const int64_t hi = (first + cnt < n_entries) ? entries[first + cnt].dst_offset : bucket_numel;
+    PackTable t;
+    memset(&t, 0, sizeof(t));
+    t.n = cnt;
+    const size_t esz = src_dtype == HOD_DTYPE_BF16 ? 2 : 4;
+    for (int i = 0; i < cnt; ++i) {
+      const hod_pack_entry& e = entries[first + i];
+      t.off[i] = e.dst_offset - lo;
+      t.numel[i] = e.numel;
+      // the vector path reads 8 elements at (tile_start - off) which is a
+      // multiple of 8 only when off is; require both for the fast path
+      const bool ok = aligned16(e.src) && ((e.dst_offset - lo) % 8 == 0) && (esz * 8) % 16 == 0;
+      t.src[i] = e.src;
+      if (ok) t.vec_ok |= (1ull << i);
+    }
+    const int64_t span = hi - lo;
+    if (span > 0) {
+      if (!aligned16(bucket + lo)) {
+        set_error("hod_pack_bf16: window start %lld not 16-byte aligned", (long long)lo); return HOD_EALIGN;
+      }
+      const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, 4);
+      if (src_dtype == HOD_DTYPE_BF16)
+        pack_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
+      else
+        pack_kernel<float><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
+      const int rc = cuda_status(cudaGetLastError(), "hod_pack_bf16 launch");
+      if (rc) return rc;
+    }
+    first += cnt;
+  } while (first < n_entries);
+  return HOD_OK;
+}
+
+int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) {
+  if (!partials || n < 0 || (n > 0 && !x)) { set_error("hod_sumsq_bf16: bad arguments"); return HOD_EINVAL; }
+  sumsq_kernel<<<HOD_SUMSQ_PARTIALS, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
+  return cuda_status(cudaGetLastError(), "hod_sumsq_bf16 launch");
+}
+
+int hod_sum_partials(const float* partials, int64_t n_partials, float* out, void* stream) {
+  if (!partials || !out || n_partials < 0) { set_error("hod_sum_partials: bad arguments"); return HOD_EINVAL; }
+  sum_partials_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(partials, n_partials, out);
+  return cuda_status(cudaGetLastError(), "hod_sum_partials launch");
+}
+
+int hod_clip_coef(const float* sumsq, float max_norm, float* coef, float* norm, void* stream) {
+  if (!sumsq || !coef || !(max_norm > 0.0f)) { set_error("hod_clip_coef: bad arguments"); return HOD_EINVAL; }
+  clip_coef_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sumsq, max_norm, coef, norm);
+  return cuda_status(cudaGetLastError(), "hod_clip_coef launch");
+}
+
+int hod_adamw_bf16(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* grad,
+                   uint16_t* param, int64_t n, const hod_adamw_params* hp, const float* clip_coef,
+                   void* stream) {
+  return launch_adamw<uint16_t>(master, exp_avg, exp_avg_sq, grad, param, n, hp, clip_coef,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int hod_adamw_f32(float* master, float* exp_avg, float* exp_avg_sq, const float* grad,
+                  uint16_t* param, int64_t n, const hod_adamw_params* hp, const float* clip_coef,
+                  void* stream) {
+  return launch_adamw<float>(master, exp_avg, exp_avg_sq, grad, param, n, hp, clip_coef,
+                             static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,369 @@
+"""The Overlapped Distributed Optimizer: host side of the B200 data path.
+
+Per bucket b:
+
+    K1 pack/cast(b)  ->  C1 reduce-scatter(b)  ->  [K3 sumsq(b)]
+                     ->  K2 AdamW(shard b)     ->  C2 all-gather(b)
+
+K1 runs on a pack stream as soon as bucket b's gradients are ready (either
+``grad_ready`` calls from backward hooks, or ``step(grads)``), the
+collectives run on a communication stream and the update on an optimizer
+stream; CUDA events carry every dependency, the host never synchronises.
+With gradient clipping the update of every bucket waits for the global norm
+(K3 partials -> C3 all-reduce -> clip coefficient in device memory).
+
+This replaces the reference's *priced* DP synchronisation — reduce-scatter
+plus all-gather of the stage's gradient bytes charged after the pipeline
+flush (simulator.py:327-333, 445-452) — with the real,
+overlapped operation.  The ``backend`` selects how C1/C2 move bytes:
+
+* ``"nccl"`` — NCCL ReduceScatter / AllGather (bf16, sum) over NVLink; the
+  library baseline.
+* ``"none"`` — d == 1: no collective, AdamW reads the packed bucket.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _native as nat
+from .buckets import BucketLayout, build_bucket_layout
+from .comm import DPGroup, NcclComm
+from .errors import InfeasibleConfigError
+
+_BF16 = torch.bfloat16
+
+
+@dataclass
+class StepReport:
+    """What one ``step`` did.  Device-side values stay on the device until
+    ``resolve()`` is called (after the caller synchronises)."""
+
+    step: int
+    buckets: int
+    params_updated: int           # elements of this rank's shards updated
+    grad_norm: torch.Tensor | None = None
+    clip_coef: torch.Tensor | None = None
+    start: torch.cuda.Event | None = None
+    end: torch.cuda.Event | None = None
+    resolved: dict = field(default_factory=dict)
+
+    def resolve(self) -> dict:
+        if not self.resolved:
+            doc = {"step": self.step, "buckets": self.buckets,
+                   "params_updated": self.params_updated}
+            if self.start is not None and self.end is not None:
+                doc["step_ms"] = self.start.elapsed_time(self.end)
+            if self.grad_norm is not None:
+                doc["grad_norm"] = float(self.grad_norm.item())
+                doc["clip_coef"] = float(self.clip_coef.item())
+            self.resolved = doc
+        return self.resolved
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+class DistributedOptimizer:
+    """Sharded, bucketed, overlapped AdamW over one DP row.
+
+    Parameters
+    ----------
+    init_params : list of tensors (registration order) giving the initial
+        values; their dtype may be fp32 (exact master init) or bf16.
+    dp_group : DPGroup of this rank (``DPGroup.from_plan(plan, rank)`` maps a
+        reference GroupPlan DP row); ``None`` means a single rank.
+    norm_ranks : ranks over which the clip norm is summed (default: the DP
+        row; the whole world for PP x DP so every stage sees one norm).
+    grad_scale : multiplier fused into the pack (default 1/d: gradient mean).
+    """
+
+    def __init__(self, init_params, *, lr: float = 1e-4, betas=(0.9, 0.95), eps: float = 1e-8,
+                 weight_decay: float = 0.1, clip: float | None = None,
+                 bucket_size: int = 25_000_000, dp_group: DPGroup | None = None,
+                 norm_ranks=None, grad_scale: float | None = None, backend: str = "auto",
+                 device=None, param_align: int = 64):
+        if clip is not None and not clip > 0:
+            raise InfeasibleConfigError(f"clip must be positive, got {clip}")
+        self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
+                       else torch.device(device))
+        self.lr, self.betas, self.eps, self.weight_decay = lr, tuple(betas), eps, weight_decay
+        self.clip = clip
+        self.group = dp_group or DPGroup.single(0)
+        self.dp = self.group.size
+        self.shard_index = self.group.index
+        self.grad_scale = (1.0 / self.dp) if grad_scale is None else float(grad_scale)
+        if backend == "auto":
+            backend = "none" if self.dp == 1 else "nccl"
+        if backend not in ("none", "nccl"):
+            raise InfeasibleConfigError(f"unknown backend {backend!r}")
+        if backend == "none" and self.dp != 1:
+            raise InfeasibleConfigError("backend 'none' needs a single-rank DP group")
+        self.backend = backend
+        nat.load()
+
+        shapes = [tuple(p.shape) for p in init_params]
+        numels = [math.prod(s) for s in shapes]
+        self.layout: BucketLayout = build_bucket_layout(numels, bucket_size, self.dp, param_align)
+        L = self.layout
+        total = L.total_numel
+        dev = self.device
+        self.param_buffer = torch.zeros(total, dtype=_BF16, device=dev)
+        self.grad_buffer = torch.empty(total, dtype=_BF16, device=dev)
+        shard_total = total // self.dp
+        self.master = torch.empty(shard_total, dtype=torch.float32, device=dev)
+        self.exp_avg = torch.zeros(shard_total, dtype=torch.float32, device=dev)
+        self.exp_avg_sq = torch.zeros(shard_total, dtype=torch.float32, device=dev)
+        self._shard_off = L.shard_offsets()
+
+        # model-visible bf16 params are views into the flat buffer
+        self.params: list[torch.Tensor] = [None] * len(shapes)  # type: ignore[list-item]
+        master_full = torch.zeros(total, dtype=torch.float32, device=dev) if self.dp == 1 else None
+        for b in L.buckets:
+            for s in b.slots:
+                lo = b.start + s.offset
+                view = self.param_buffer[lo:lo + s.numel].view(shapes[s.index])
+                src = init_params[s.index].detach().to(dev)
+                view.copy_(src.to(_BF16))
+                self.params[s.index] = view
+                if master_full is not None:
+                    master_full[lo:lo + s.numel].copy_(src.reshape(-1).float())
+        if master_full is not None:
+            self.master.copy_(master_full)
+            del master_full
+        else:
+            for b, off in zip(L.buckets, self._shard_off):
+                lo, hi = b.shard_range(self.shard_index, self.dp)
+                seg = torch.zeros(hi - lo, dtype=torch.float32, device=dev)
+                for s in b.slots:
+                    a, e = b.start + s.offset, b.start + s.offset + s.numel
+                    x0, x1 = max(a, lo), min(e, hi)
+                    if x0 < x1:
+                        seg[x0 - lo:x1 - lo] = init_params[s.index].detach().reshape(-1)[x0 - a:x1 - a].to(dev).float()
+                self.master[off:off + (hi - lo)].copy_(seg)
+
+        # streams / events (one set per bucket, reused every step)
+        self.s_pack = torch.cuda.Stream(device=dev)
+        self.s_comm = torch.cuda.Stream(device=dev) if self.dp > 1 else self.s_pack
+        self.s_opt = torch.cuda.Stream(device=dev) if self.dp > 1 else self.s_pack
+        nb = len(L.buckets)
+        self._ev_packed = [torch.cuda.Event() for _ in range(nb)]
+        self._ev_reduced = [torch.cuda.Event() for _ in range(nb)]
+        self._ev_updated = [torch.cuda.Event() for _ in range(nb)]
+        self._ev_params = [torch.cuda.Event() for _ in range(nb)]
+        self._ev_norm = torch.cuda.Event()
+        self._ev_start = torch.cuda.Event(enable_timing=True)
+        self._ev_end = torch.cuda.Event(enable_timing=True)
+
+        if self.clip is not None:
+            self._partials = torch.zeros(nb * nat.HOD_SUMSQ_PARTIALS, dtype=torch.float32, device=dev)
+            self._sumsq = torch.zeros(1, dtype=torch.float32, device=dev)
+            self._coef = torch.ones(1, dtype=torch.float32, device=dev)
+            self._norm = torch.zeros(1, dtype=torch.float32, device=dev)
+
+        # communicators
+        self.comm = None
+        self.norm_comm = None
+        if self.backend == "nccl":
+            self.comm = NcclComm(self.group.ranks, self.group.global_rank, "dp")
+        norm_ranks = tuple(norm_ranks) if norm_ranks is not None else self.group.ranks
+        self.norm_ranks = norm_ranks
+        if self.clip is not None and len(norm_ranks) > 1:
+            self.norm_comm = (self.comm if norm_ranks == self.group.ranks and self.comm is not None
+                              else NcclComm(norm_ranks, self.group.global_rank, "norm"))
+
+        self.step_count = 0
+        self._pending_grads: list[dict[int, torch.Tensor]] = []
+        self._launched: list[bool] = []
+        self._deferred_ag: list[int] = []
+        self._in_step = False
+
+    # ------------------------------------------------------------------ API
+    def bucket_layout(self) -> BucketLayout:
+        return self.layout
+
+    def begin_step(self) -> None:
+        if self._in_step:
+            raise InfeasibleConfigError("begin_step called twice without finish_step")
+        self._in_step = True
+        self.step_count += 1
+        nb = len(self.layout.buckets)
+        self._pending_grads = [dict() for _ in range(nb)]
+        self._launched = [False] * nb
+        self._deferred_ag = []
+        self._ev_start.record(torch.cuda.current_stream(self.device))
+
+    def grad_ready(self, param_index: int, grad: torch.Tensor) -> None:
+        """Backward produced ``grad`` for parameter ``param_index`` (call from a
+        post-accumulate-grad hook).  Launches the bucket once it is complete."""
+        slot = self.layout.slot(param_index)
+        pend = self._pending_grads[slot.bucket]
+        pend[param_index] = grad
+        b = self.layout.buckets[slot.bucket]
+        if len(pend) == len(b.slots):
+            self._launch_bucket(slot.bucket)
+
+    def finish_step(self) -> StepReport:
+        """Launch whatever is left, run the clip barrier if needed, and return."""
+        L = self.layout
+        for b in range(len(L.buckets)):
+            if not self._launched[b]:
+                missing = [s.index for s in L.buckets[b].slots if s.index not in self._pending_grads[b]]
+                raise InfeasibleConfigError(f"bucket {b} is missing gradients for params {missing[:8]}")
+        if self.clip is not None:
+            self._clip_and_update()
+        else:
+            self._flush_deferred_ag()
+        cur = torch.cuda.current_stream(self.device)
+        for ev in self._ev_params:
+            cur.wait_event(ev)
+        self._ev_end.record(cur)
+        self._in_step = False
+        rep = StepReport(self.step_count, len(L.buckets), L.total_numel // self.dp,
+                         start=self._ev_start, end=self._ev_end)
+        if self.clip is not None:
+            rep.grad_norm, rep.clip_coef = self._norm, self._coef
+        return rep
+
+    def step(self, grads) -> StepReport:
+        """One optimizer step over ``grads`` (registration order), issued in
+        backward order as if every gradient had just become ready."""
+        self.begin_step()
+        for b in self.layout.buckets:
+            for s in b.slots:
+                self.grad_ready(s.index, grads[s.index])
+        return self.finish_step()
+
+    def wait_params(self, bucket: int, stream=None) -> None:
+        """Make ``stream`` (default: current) wait until bucket's params are gathered."""
+        (stream or torch.cuda.current_stream(self.device)).wait_event(self._ev_params[bucket])
+
+    def register_hooks(self, module_params) -> list:
+        """Attach post-accumulate-grad hooks: parameter i's gradient feeds
+        ``grad_ready(i)``.  ``module_params[i]`` must be the model parameter
+        for registration index i."""
+        handles = []
+        for i, p in enumerate(module_params):
+            def hook(param, i=i):
+                self.grad_ready(i, param.grad)
+            handles.append(p.register_post_accumulate_grad_hook(hook))
+        return handles
+
+    def close(self) -> None:
+        for c in {id(x): x for x in (self.comm, self.norm_comm) if x is not None}.values():
+            c.close()
+        self.comm = self.norm_comm = None
+
+    # ------------------------------------------------------------ internals
+    def _hp(self) -> nat.AdamWParams:
+        return nat.AdamWParams(self.lr, self.betas[0], self.betas[1], self.eps, self.weight_decay,
+                               self.step_count)
+
+    def _grad_shard(self, b) -> tuple[int, int]:
+        """(ptr, numel) of this rank's reduced-gradient shard of bucket b."""
+        lo, hi = b.shard_range(self.shard_index, self.dp)
+        return _ptr(self.grad_buffer) + 2 * lo, hi - lo
+
+    def _launch_bucket(self, bi: int) -> None:
+        b = self.layout.buckets[bi]
+        grads = self._pending_grads[bi]
+        cur = torch.cuda.current_stream(self.device)
+        self.s_pack.wait_stream(cur)
+        # keep gradient memory alive until the pack has consumed it
+        for s in b.slots:
+            g = grads[s.index]
+            if g.numel() != s.numel:
+                raise InfeasibleConfigError(
+                    f"gradient for param {s.index} has {g.numel()} elements, expected {s.numel}")
+            g.record_stream(self.s_pack)
+        first = grads[b.slots[0].index]
+        if first.dtype == torch.float32:
+            dtype = nat.HOD_DTYPE_F32
+        elif first.dtype == _BF16:
+            dtype = nat.HOD_DTYPE_BF16
+        else:
+            raise InfeasibleConfigError(f"gradient dtype {first.dtype} not supported (bf16/fp32)")
+        entries = (nat.PackEntry * len(b.slots))()
+        for k, s in enumerate(b.slots):
+            g = grads[s.index]
+            if not g.is_contiguous() or g.dtype != first.dtype:
+                raise InfeasibleConfigError(f"gradient {s.index} must be contiguous {first.dtype}")
+            entries[k].src = _ptr(g)
+            entries[k].numel = s.numel
+            entries[k].dst_offset = s.offset
+        bucket_ptr = _ptr(self.grad_buffer) + 2 * b.start
+        nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
+                 ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
+        self._ev_packed[bi].record(self.s_pack)
+        self._launched[bi] = True
+
+        reduced = self._ev_packed[bi]
+        if self.backend == "nccl":
+            self.s_comm.wait_event(self._ev_packed[bi])
+            shard_ptr, shard_n = self._grad_shard(b)
+            self.comm.reduce_scatter_bf16(bucket_ptr, shard_ptr, shard_n, self.s_comm)
+            self._ev_reduced[bi].record(self.s_comm)
+            reduced = self._ev_reduced[bi]
+
+        if self.clip is not None:
+            shard_ptr, shard_n = self._grad_shard(b)
+            part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * bi
+            nat.call("hod_sumsq_bf16", shard_ptr, shard_n, part, nat.stream_ptr(self.s_comm))
+        else:
+            self._update_bucket(bi, reduced, clip_coef_ptr=None)
+            # all-gather of the previous bucket goes behind this RS (pipelining)
+            self._flush_deferred_ag(keep_last=True)
+
+    def _update_bucket(self, bi: int, ready: torch.cuda.Event, clip_coef_ptr) -> None:
+        b = self.layout.buckets[bi]
+        self.s_opt.wait_event(ready)
+        shard_ptr, shard_n = self._grad_shard(b)
+        lo, _ = b.shard_range(self.shard_index, self.dp)
+        off = self._shard_off[bi]
+        hp = self._hp()
+        nat.call("hod_adamw_bf16", _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
+                 _ptr(self.exp_avg_sq) + 4 * off, shard_ptr, _ptr(self.param_buffer) + 2 * lo,
+                 shard_n, ctypes.byref(hp), clip_coef_ptr, nat.stream_ptr(self.s_opt))
+        self._ev_updated[bi].record(self.s_opt)
+        if self.backend == "nccl":
+            self._deferred_ag.append(bi)
+        else:
+            self._ev_params[bi].record(self.s_opt)
+
+    def _issue_ag(self, bi: int) -> None:
+        b = self.layout.buckets[bi]
+        self.s_comm.wait_event(self._ev_updated[bi])
+        lo, hi = b.shard_range(self.shard_index, self.dp)
+        self.comm.all_gather_bf16(_ptr(self.param_buffer) + 2 * lo, _ptr(self.param_buffer) + 2 * b.start,
+                                  hi - lo, self.s_comm)
+        self._ev_params[bi].record(self.s_comm)
+
+    def _flush_deferred_ag(self, keep_last: bool = False) -> None:
+        while len(self._deferred_ag) > (1 if keep_last else 0):
+            self._issue_ag(self._deferred_ag.pop(0))
+
+    def _clip_and_update(self) -> None:
+        nb = len(self.layout.buckets)
+        s = self.s_comm
+        nat.call("hod_sum_partials", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS,
+                 _ptr(self._sumsq), nat.stream_ptr(s))
+        if self.norm_comm is not None:
+            self.norm_comm.all_reduce_f32(_ptr(self._sumsq), 1, s)
+        nat.call("hod_clip_coef", _ptr(self._sumsq), ctypes.c_float(self.clip), _ptr(self._coef),
+                 _ptr(self._norm), nat.stream_ptr(s))
+        self._ev_norm.record(s)
+        for bi in range(nb):
+            self._update_bucket(bi, self._ev_norm, clip_coef_ptr=_ptr(self._coef))
+            if self.backend == "nccl" and len(self._deferred_ag) > 1:
+                self._issue_ag(self._deferred_ag.pop(0))
+        self._flush_deferred_ag()
+
+    # ------------------------------------------------------------ helpers
+    def full_master(self) -> torch.Tensor:
+        """This rank's fp32 master shards, concatenated (debug / checkpoint)."""
+        return self.master

@@ -1,0 +1,89 @@
+"""DistributedOptimizer (d = 1 on one GPU) vs the oracle's whole-step restatement.
+
+Multi-rank parity (d = 2/4/8) lives in tests/test_multigpu_gpu.py.
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_2312_03549_b200 import DistributedOptimizer  # noqa: E402
+from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
+from paper_2312_03549_b200.synthetic import init_params, make_grads  # noqa: E402
+
+DEV = "cuda"
+
+
+def u16(t):
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _oracle_state(oracle, layout, params_cpu):
+    """Per-bucket [(master, m, v)] for a single rank from fp32 initial params."""
+    state = []
+    for b in layout.buckets:
+        flat = np.zeros(b.numel, np.float32)
+        for s in b.slots:
+            flat[s.offset:s.offset + s.numel] = params_cpu[s.index].reshape(-1)
+        state.append([(flat, np.zeros(b.numel, np.float32), np.zeros(b.numel, np.float32))])
+    return state
+
+
+@pytest.mark.parametrize("config,grad_dtype,clip,bucket",
+                         [("toy", torch.float32, None, 25_000_000),
+                          ("toy", torch.bfloat16, 1.0, 2_000_000),
+                          ("odd", torch.bfloat16, 0.01, 100_000),
+                          ("odd", torch.float32, None, 10**9)])
+def test_single_rank_steps_match_oracle(oracle, native, config, grad_dtype, clip, bucket):
+    gs = config_gradset(config)
+    p0 = init_params(gs, DEV)
+    opt = DistributedOptimizer(p0, bucket_size=bucket, clip=clip)
+    L = opt.layout
+    state = _oracle_state(oracle, L, [p.cpu().numpy() for p in p0])
+    for step in (1, 2, 3):
+        grads = make_grads(gs, step, 0, DEV, dtype=grad_dtype)
+        rep = opt.step(grads)
+        torch.cuda.synchronize()
+        gcpu = [[g.cpu().numpy() if grad_dtype == torch.float32 else u16(g) for g in grads]]
+        params, norm = oracle.step_all_ranks(gcpu, [
+            {"params": [(s.index, s.offset, s.numel) for s in b.slots], "numel": b.numel}
+            for b in L.buckets], state, step, opt.lr, opt.betas, opt.eps, opt.weight_decay,
+            clip=clip)
+        if clip is not None:
+            got = rep.resolve()
+            assert abs(got["grad_norm"] - norm) <= 1e-5 * norm
+            # the coefficient the device used is fed back: AdamW parity is exact
+        pb = u16(opt.param_buffer)
+        for bi, b in enumerate(L.buckets):
+            master, m, v = state[bi][0]
+            off = L.shard_offsets()[bi]
+            dev_master = opt.master[off:off + b.numel].cpu().numpy()
+            if clip is None:
+                np.testing.assert_array_equal(pb[b.start:b.start + b.numel], params[bi])
+                np.testing.assert_array_equal(dev_master, master)
+            else:
+                # clip coefficient differs by <= 1 ulp (norm order) => 1e-6 relative
+                np.testing.assert_allclose(dev_master, master, rtol=1e-6, atol=1e-6 * np.abs(master).max())
+                np.testing.assert_allclose(opt.exp_avg[off:off + b.numel].cpu().numpy(), m,
+                                           rtol=1e-6, atol=1e-6 * np.abs(m).max())
+        # model views alias the flat buffer
+        for i, p in enumerate(opt.params):
+            s = L.slot(i)
+            b = L.buckets[s.bucket]
+            assert p.data_ptr() == opt.param_buffer.data_ptr() + 2 * (b.start + s.offset)
+    opt.close()
+
+
+def test_padding_stays_zero_and_params_alias(native):
+    gs = config_gradset("odd")
+    opt = DistributedOptimizer(init_params(gs, DEV), bucket_size=50_000)
+    opt.step(make_grads(gs, 1, 0, DEV))
+    torch.cuda.synchronize()
+    pad_mask = torch.ones(opt.layout.total_numel, dtype=torch.bool, device=DEV)
+    for b in opt.layout.buckets:
+        for s in b.slots:
+            pad_mask[b.start + s.offset:b.start + s.offset + s.numel] = False
+    assert torch.count_nonzero(opt.grad_buffer[pad_mask]).item() == 0
+    assert torch.count_nonzero(opt.param_buffer[pad_mask]).item() == 0
