@@ -1,0 +1,376 @@
+#!/usr/bin/env python
+"""Optimizer-step benchmark: BASELINE.json metric on B200.
+
+``python bench.py [--gpus N] [--steps K] [--warmup W] [--config gpt1.3b]``
+(one process per GPU; for N > 1 launch under torch.distributed.run).
+
+A step is one Overlapped Distributed Optimizer step over one synthetic
+gradient set: per bucket pack/cast -> reduce-scatter ->
+sharded AdamW -> all-gather.  ``value`` = parameters updated per second for
+the whole job (every parameter of the set is updated once per step, the
+shards of all N ranks together) with inputs resident in HBM; ``e2e`` is the
+same metric through ``DistributedOptimizer.step`` fed from pinned HOST
+gradients (H2D inside the timed region) with a device->host read of the
+step result.  ``--impl reference`` times the CPU restatement of the same
+step (the reference has no optimizer of its own) on the host
+cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "optimizer-step params/s"
+UNIT = "params/s"
+CONFIGS = {
+    "toy": dict(grad_dtype="f32", clip=None, desc="toy GPT L4 h256 V51200, fp32 grads"),
+    "gpt1.3b": dict(grad_dtype="bf16", clip=None, desc="GPT-3 1.3B-shape gradient set (L24 h2048 V51200), bf16 grads, fp32 master AdamW"),
+    "llama7b": dict(grad_dtype="bf16", clip=1.0, desc="LLaMA-7B real tensor list, bf16 grads, grad-norm clip 1.0"),
+}
+FALLBACK_HBM_GBS = 6650.0
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling DURING the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except FileNotFoundError:
+            self.proc = None
+        time.sleep(0.25)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_setup(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def _barrier(world):
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _sum_over_ranks(x: float, world: int) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if world == 1:
+        return x
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t)
+    return float(t.item())
+
+
+def _traffic_from_profile(kernel: str):
+    """dram bytes per launch of ``kernel`` from the committed ncu summary."""
+    for p in sorted((ROOT / "profiles").glob("*ncu_summary.json"), reverse=True):
+        try:
+            d = json.loads(p.read_text())
+        except Exception:
+            continue
+        k = d.get("kernels", {}).get(kernel)
+        if k and k.get("dram_bytes_per_launch"):
+            return k["dram_bytes_per_launch"], k.get("algorithmic_bytes_per_launch"), p.name
+    return None, None, None
+
+
+def cpu_baseline(config: str, gs, seconds: float = 10.0) -> dict:
+    """Oracle (CPU port) timed on a bounded sample: pack + AdamW over whole
+    buckets of the workload, repeated until ``seconds`` elapse."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2312_03549_b200.buckets import build_bucket_layout
+
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    L = build_bucket_layout(gs.numels, 25_000_000, dp=1)
+    b = max(L.buckets, key=lambda x: -x.numel)  # smallest whole bucket
+    rng = np.random.default_rng(0)
+    grads = [oracle.f32_to_bf16(rng.standard_normal(s.numel, dtype=np.float32) * 1e-3) for s in b.slots]
+    master = (rng.standard_normal(b.numel, dtype=np.float32) * 0.02)
+    m = np.zeros(b.numel, np.float32)
+    v = np.zeros(b.numel, np.float32)
+    offs = [s.offset for s in b.slots]
+    done, t0, step = 0, time.perf_counter(), 0
+    while True:
+        step += 1
+        bucket = oracle.pack(grads, offs, b.numel, 1.0)
+        oracle.adamw(master, m, v, bucket, step)
+        done += b.numel
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": oracle.threads(), "kind": "port",
+            "sample": f"{step} x (pack + AdamW) over one {b.numel}-element bucket of {config} "
+                      f"(d=1 step restated by oracle/hod_oracle.c, OpenMP {oracle.threads()} threads, {dt:.1f} s)"}
+
+
+def run_reference(args) -> None:
+    """--impl reference: the CPU restatement of the same step on host cores."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_2312_03549_b200.gradsets import config_gradset
+
+    gs = config_gradset(args.config)
+    times = []
+    base = None
+    for i in range(args.warmup + args.steps):
+        r = cpu_baseline(args.config, gs, seconds=max(1.0, args.ref_seconds / max(1, args.steps)))
+        if i >= args.warmup:
+            times.append(r["value"])
+            base = r
+    value = statistics.median(times)
+    total = gs.total
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "impl": "reference",
+        "config": {"workload": CONFIGS[args.config]["desc"], "params": total, "bucket_size": 25_000_000,
+                   "world": world, "note": "reference has no optimizer (SPEC.md:14); CPU restatement timed"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
+                         "sample": base["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args) -> None:
+    import torch
+
+    from paper_2312_03549_b200 import DistributedOptimizer, _native
+    from paper_2312_03549_b200.comm import DPGroup
+    from paper_2312_03549_b200.gradsets import config_gradset
+    from paper_2312_03549_b200.synthetic import init_params, make_grads
+
+    world, rank, local = _dist_setup(args)
+    cfg = CONFIGS[args.config]
+    clip = cfg["clip"] if args.clip is None else (None if args.clip <= 0 else args.clip)
+    gs = config_gradset(args.config)
+    dev = torch.device("cuda", local)
+    gdtype = torch.float32 if cfg["grad_dtype"] == "f32" else torch.bfloat16
+
+    p0 = init_params(gs, dev)
+    group = DPGroup(tuple(range(world)), rank)
+    opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group,
+                               backend=args.backend)
+    del p0
+    torch.cuda.empty_cache()
+    grads = make_grads(gs, 1, rank, dev, dtype=gdtype)
+
+    # ---- device-resident timed region -------------------------------------
+    for _ in range(args.warmup):
+        opt.step(grads)
+    _barrier(world)
+    clocks = ClockSampler(local)
+    clocks.start()
+    opt.enable_kernel_timing(True)
+    launches0 = _native.launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _barrier(world)
+    start.record()
+    for _ in range(args.steps):
+        opt.step(grads)
+    end.record()
+    torch.cuda.synchronize()
+    launches = _native.launch_count() - launches0
+    _barrier(world)
+    clk = clocks.stop()
+    ms = start.elapsed_time(end) / args.steps
+    ms = _max_over_ranks(ms, world)
+    kt = opt.kernel_timing()
+    opt.enable_kernel_timing(False)
+    params_per_step = gs.total  # every parameter of the set updated once per step
+    value = params_per_step / (ms / 1e3)
+
+    # ---- roofline of the dominant kernel (AdamW) --------------------------
+    peak, peak_src = _peaks()
+    n_launch, ktime, kbytes = kt.get("adamw", (0, 0.0, 0))
+    achieved = (kbytes / (ktime / 1e3)) / 1e9 if ktime > 0 else None
+    traffic, alg_per_launch, prof = _traffic_from_profile("adamw")
+    roof = {"kernel": "hod adamw_vec_kernel (K2)", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic, "traffic_source": prof, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": kbytes / max(1, n_launch),
+            "avg_launch_ms": ktime / max(1, n_launch), "launches_timed": n_launch,
+            "bytes_per_element": 28}
+    kernels = {k: {"launches": n, "ms_total": t, "GBps": (b / (t / 1e3)) / 1e9 if t else None}
+               for k, (n, t, b) in kt.items()}
+    # step-level roofline: max(HBM bytes / peak, NVLink bytes / 900 GB/s)
+    d = world
+    P = params_per_step
+    src_b = 4 if gdtype == torch.float32 else 2
+    hbm_bytes = (src_b + 2) * P + 28 * P / d + (2 * P / d if clip else 0)
+    nvl_bytes = 4 * P * (d - 1) / d
+    t_roof = max(hbm_bytes / (peak * 1e9), nvl_bytes / 900e9)
+    step_roof = {"t_roof_ms": t_roof * 1e3, "frac": (t_roof * 1e3) / ms,
+                 "hbm_bytes_per_gpu": hbm_bytes, "nvlink_bytes_per_gpu_per_dir": nvl_bytes,
+                 "bound": "hbm" if hbm_bytes / (peak * 1e9) >= nvl_bytes / 900e9 else "nvlink"}
+
+    # ---- e2e through the public API with host buffers ---------------------
+    e2e = None
+    if not args.no_e2e:
+        host = [g.cpu().pin_memory() for g in grads]
+        res_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        del grads
+        torch.cuda.empty_cache()
+        for _ in range(max(1, min(args.warmup, 2))):
+            opt.step(host)
+        _barrier(world)
+        e_steps = max(1, min(args.steps, 5))
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(e_steps):
+            rep = opt.step(host)
+            # device->host read of the step result: grad norm (clip) or first updated param
+            src = rep.grad_norm if rep.grad_norm is not None else opt.params[0].reshape(-1)[:2].view(torch.float32)
+            res_host.copy_(src, non_blocking=True)
+        t1.record()
+        torch.cuda.synchronize()
+        ems = _max_over_ranks(t0.elapsed_time(t1) / e_steps, world)
+        h2d = _sum_over_ranks(float(sum(h.numel() * h.element_size() for h in host)), world)
+        e2e = {"value": params_per_step / (ems / 1e3), "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4 * world,
+               "steps": e_steps, "path": "DistributedOptimizer.step(pinned host grads)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, gs, seconds=args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16-grads/f32-adamw", "data": "synthetic",
+            "config": {"workload": cfg["desc"], "config": args.config, "params": P,
+                       "buckets": len(opt.layout.buckets), "bucket_size": args.bucket_size,
+                       "dp": world, "clip": clip, "backend": opt.backend,
+                       "l2": "inputs (~%.0f GB) >> 126 MB L2, no flush needed" % (hbm_bytes / 1e9)},
+            "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    opt.close()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--bucket-size", type=int, default=25_000_000)
+    ap.add_argument("--backend", default="auto")
+    ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--ref-seconds", type=float, default=30.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -78,6 +78,8 @@ typedef struct hod_adamw_params {
 /* ---- version / errors ---------------------------------------------------- */
 int hod_abi_version(void);
 const char* hod_last_error(void);
+/* number of kernels this library has launched in the process (all streams) */
+long long hod_launch_count(void);
 
 /* ---- K1: bucket pack + dp-scale + bf16 cast ---------------
  * bucket[dst_offset + i] = bf16_rne(float(src[i]) * scale), zeros elsewhere.

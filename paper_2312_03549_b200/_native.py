@@ -22,7 +22,7 @@ HOD_DTYPE_F32 = 1
 
 # every symbol include/hod.h declares (checked by tests/test_abi.py)
 EXPORTED = (
-    "hod_abi_version", "hod_last_error",
+    "hod_abi_version", "hod_last_error", "hod_launch_count",
     "hod_pack_bf16", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
     "hod_adamw_bf16", "hod_adamw_f32",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
@@ -61,6 +61,7 @@ def load(build_if_missing: bool = True):
     sig = {
         "hod_abi_version": ([], I),
         "hod_last_error": ([], ctypes.c_char_p),
+        "hod_launch_count": ([], ctypes.c_longlong),
         "hod_pack_bf16": ([ctypes.POINTER(PackEntry), I, P, I64, F, I, P], I),
         "hod_sumsq_bf16": ([P, I64, P, P], I),
         "hod_sum_partials": ([P, I64, P, P], I),
@@ -90,6 +91,11 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def launch_count() -> int:
+    """Kernels launched by libhod.so so far in this process."""
+    return int(load().hod_launch_count())
 
 
 def stream_ptr(stream) -> int:

@@ -17,6 +17,7 @@ namespace hod {
 // Thread-local error slot behind hod_last_error().
 void set_error(const char* fmt, ...);
 int cuda_status(cudaError_t e, const char* what);
+void count_launch(int n);  // feeds hod_launch_count()
 
 constexpr int kThreads = 256;
 constexpr int kSMs = 148;

@@ -9,11 +9,16 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <atomic>
+
 #include "hod_common.cuh"
 
 namespace hod {
 
 static thread_local char g_err[512] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -200,6 +205,7 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
     const int64_t n_vec = n / 8;
     if (n_vec > 0) {
       const int grid = grid_for(n_vec, kThreads);
+      count_launch(1);
       if (clip_coef)
         adamw_vec_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef);
       else
@@ -209,6 +215,7 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
   }
   if (done < n) {
     const int grid = grid_for(n - done, kThreads);
+    count_launch(1);
     if (clip_coef)
       adamw_scalar_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, clip_coef);
     else
@@ -282,6 +289,8 @@ int hod_abi_version(void) { return HOD_ABI_VERSION; }
 
 const char* hod_last_error(void) { return g_err; }
 
+long long hod_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket,
                   int64_t bucket_numel, float scale, int src_dtype, void* stream) {
   if (!bucket || bucket_numel < 0 || n_entries < 0 || (n_entries > 0 && !entries)) {
@@ -329,6 +338,7 @@ int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket
         set_error("hod_pack_bf16: window start %lld not 16-byte aligned", (long long)lo); return HOD_EALIGN;
       }
       const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, 4);
+      count_launch(1);
       if (src_dtype == HOD_DTYPE_BF16)
         pack_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
       else
@@ -343,18 +353,21 @@ int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket
 
 int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) {
   if (!partials || n < 0 || (n > 0 && !x)) { set_error("hod_sumsq_bf16: bad arguments"); return HOD_EINVAL; }
+  count_launch(1);
   sumsq_kernel<<<HOD_SUMSQ_PARTIALS, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
   return cuda_status(cudaGetLastError(), "hod_sumsq_bf16 launch");
 }
 
 int hod_sum_partials(const float* partials, int64_t n_partials, float* out, void* stream) {
   if (!partials || !out || n_partials < 0) { set_error("hod_sum_partials: bad arguments"); return HOD_EINVAL; }
+  count_launch(1);
   sum_partials_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(partials, n_partials, out);
   return cuda_status(cudaGetLastError(), "hod_sum_partials launch");
 }
 
 int hod_clip_coef(const float* sumsq, float max_norm, float* coef, float* norm, void* stream) {
   if (!sumsq || !coef || !(max_norm > 0.0f)) { set_error("hod_clip_coef: bad arguments"); return HOD_EINVAL; }
+  count_launch(1);
   clip_coef_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sumsq, max_norm, coef, norm);
   return cuda_status(cudaGetLastError(), "hod_clip_coef launch");
 }

@@ -177,6 +177,8 @@ class DistributedOptimizer:
             self.norm_comm = (self.comm if norm_ranks == self.group.ranks and self.comm is not None
                               else NcclComm(norm_ranks, self.group.global_rank, "norm"))
 
+        self._ktiming = None
+        self._staging = None
         self.step_count = 0
         self._pending_grads: list[dict[int, torch.Tensor]] = []
         self._launched: list[bool] = []
@@ -233,11 +235,29 @@ class DistributedOptimizer:
     def step(self, grads) -> StepReport:
         """One optimizer step over ``grads`` (registration order), issued in
         backward order as if every gradient had just become ready."""
+        host = grads[0].device.type == "cpu"
+        if host:
+            self._ensure_staging(grads)
         self.begin_step()
         for b in self.layout.buckets:
+            if host:
+                # host->device copy of this bucket's gradients on the copy
+                # engine; the pack of bucket b waits only for its own copy
+                with torch.cuda.stream(self.s_h2d):
+                    for s in b.slots:
+                        self._staging[s.index].copy_(grads[s.index], non_blocking=True)
+                self._ev_h2d[b.index].record(self.s_h2d)
+                self.s_pack.wait_event(self._ev_h2d[b.index])
             for s in b.slots:
-                self.grad_ready(s.index, grads[s.index])
+                self.grad_ready(s.index, self._staging[s.index] if host else grads[s.index])
         return self.finish_step()
+
+    def _ensure_staging(self, grads) -> None:
+        if (self._staging is not None and self._staging[0].dtype == grads[0].dtype):
+            return
+        self._staging = [torch.empty(g.shape, dtype=g.dtype, device=self.device) for g in grads]
+        self.s_h2d = torch.cuda.Stream(device=self.device)
+        self._ev_h2d = [torch.cuda.Event() for _ in self.layout.buckets]
 
     def wait_params(self, bucket: int, stream=None) -> None:
         """Make ``stream`` (default: current) wait until bucket's params are gathered."""
@@ -297,8 +317,11 @@ class DistributedOptimizer:
             entries[k].numel = s.numel
             entries[k].dst_offset = s.offset
         bucket_ptr = _ptr(self.grad_buffer) + 2 * b.start
+        t0 = self._timed_event(self.s_pack)
         nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
                  ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
+        src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
+        self._timed_close("pack", t0, self.s_pack, (src_bytes + 2) * b.numel)
         self._ev_packed[bi].record(self.s_pack)
         self._launched[bi] = True
 
@@ -326,9 +349,11 @@ class DistributedOptimizer:
         lo, _ = b.shard_range(self.shard_index, self.dp)
         off = self._shard_off[bi]
         hp = self._hp()
+        t0 = self._timed_event(self.s_opt)
         nat.call("hod_adamw_bf16", _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
                  _ptr(self.exp_avg_sq) + 4 * off, shard_ptr, _ptr(self.param_buffer) + 2 * lo,
                  shard_n, ctypes.byref(hp), clip_coef_ptr, nat.stream_ptr(self.s_opt))
+        self._timed_close("adamw", t0, self.s_opt, 28 * shard_n)
         self._ev_updated[bi].record(self.s_opt)
         if self.backend == "nccl":
             self._deferred_ag.append(bi)
@@ -362,6 +387,39 @@ class DistributedOptimizer:
             if self.backend == "nccl" and len(self._deferred_ag) > 1:
                 self._issue_ag(self._deferred_ag.pop(0))
         self._flush_deferred_ag()
+
+    # ------------------------------------------------------------ timing
+    def enable_kernel_timing(self, on: bool = True) -> None:
+        """Record CUDA events around every K1/K2 launch, on the launching
+        stream, for live per-kernel bandwidth (bench.py roofline)."""
+        self._ktiming = [] if on else None
+
+    def kernel_timing(self) -> dict:
+        """{kernel: (launches, total_ms, algorithmic_bytes)} — synchronises."""
+        out: dict = {}
+        for name, e0, e1, nbytes in self._ktiming or []:
+            e1.synchronize()
+            n, ms, by = out.get(name, (0, 0.0, 0))
+            out[name] = (n + 1, ms + e0.elapsed_time(e1), by + nbytes)
+        return out
+
+    def reset_kernel_timing(self) -> None:
+        if self._ktiming is not None:
+            self._ktiming = []
+
+    def _timed_event(self, stream):
+        if getattr(self, "_ktiming", None) is None:
+            return None
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        return ev
+
+    def _timed_close(self, name, e0, stream, nbytes) -> None:
+        if e0 is None:
+            return
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(stream)
+        self._ktiming.append((name, e0, e1, nbytes))
 
     # ------------------------------------------------------------ helpers
     def full_master(self) -> torch.Tensor:
