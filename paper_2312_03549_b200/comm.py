@@ -51,6 +51,25 @@ class DPGroup:
         raise InvalidPlanError(f"rank {global_rank} is in no DP row of the plan")
 
 
+def comm_key(tag: str, serial: int, ranks) -> str:
+    """Store key of one communicator's bootstrap (unique per member set)."""
+    return f"hod/nccl/{tag}/{serial}/{'-'.join(map(str, ranks))}"
+
+
+def exchange_unique_id(store, key: str, is_root: bool, make_id) -> bytes:
+    """Root creates the 128-byte id and publishes it; the others wait for it."""
+    if is_root:
+        raw = make_id()
+        if len(raw) != 128:
+            raise InvalidPlanError("NCCL unique id must be 128 bytes")
+        store.set(key, raw)
+        return raw
+    raw = store.get(key)
+    if len(raw) != 128:
+        raise InvalidPlanError(f"bad unique id under {key}")
+    return bytes(raw)
+
+
 def _store():
     import torch.distributed as dist
 
@@ -70,15 +89,15 @@ class NcclComm:
         self.size = len(self.ranks)
         n = NcclComm._serial.get(tag, 0)
         NcclComm._serial[tag] = n + 1
-        key = f"hod/nccl/{tag}/{n}/{'-'.join(map(str, self.ranks))}"
-        uid = (ctypes.c_uint8 * 128)()
-        store = _store()
-        if self.rank == 0:
-            nat.call("hod_nccl_unique_id", ctypes.cast(uid, ctypes.c_void_p))
-            store.set(key, bytes(uid))
-        else:
-            raw = store.get(key)
-            ctypes.memmove(uid, raw, 128)
+        key = comm_key(tag, n, self.ranks)
+
+        def make_id() -> bytes:
+            buf = (ctypes.c_uint8 * 128)()
+            nat.call("hod_nccl_unique_id", ctypes.cast(buf, ctypes.c_void_p))
+            return bytes(buf)
+
+        raw = exchange_unique_id(_store(), key, self.rank == 0, make_id)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(raw)
         handle = ctypes.c_void_p()
         nat.call("hod_nccl_comm_init", ctypes.cast(uid, ctypes.c_void_p), self.size, self.rank,
                  ctypes.byref(handle))

@@ -69,6 +69,31 @@ def _ptr(t: torch.Tensor) -> int:
     return t.data_ptr()
 
 
+def shard_pieces(layout: BucketLayout, shard_index: int):
+    """Yield (param_index, src_begin, dst_begin, length): which slice of which
+    parameter lands where in rank ``shard_index``'s concatenated fp32 shards.
+    Padding inside a shard is left untouched (zero)."""
+    offs = layout.shard_offsets()
+    for b, off in zip(layout.buckets, offs):
+        lo, hi = b.shard_range(shard_index, layout.dp)
+        for s in b.slots:
+            a = b.start + s.offset
+            x0, x1 = max(a, lo), min(a + s.numel, hi)
+            if x0 < x1:
+                yield s.index, x0 - a, off + (x0 - lo), x1 - x0
+
+
+def fill_master_shards(layout: BucketLayout, init_params, shard_index: int,
+                       master: torch.Tensor) -> torch.Tensor:
+    """Write the fp32 initial values of this rank's shards into ``master``
+    (exact for fp32 inputs).  Works on any device (CPU in the gloo tests)."""
+    master.zero_()
+    for pi, src0, dst0, n in shard_pieces(layout, shard_index):
+        flat = init_params[pi].detach().reshape(-1)
+        master[dst0:dst0 + n].copy_(flat[src0:src0 + n].to(master.device).float())
+    return master
+
+
 class DistributedOptimizer:
     """Sharded, bucketed, overlapped AdamW over one DP row.
 
@@ -123,29 +148,13 @@ class DistributedOptimizer:
 
         # model-visible bf16 params are views into the flat buffer
         self.params: list[torch.Tensor] = [None] * len(shapes)  # type: ignore[list-item]
-        master_full = torch.zeros(total, dtype=torch.float32, device=dev) if self.dp == 1 else None
         for b in L.buckets:
             for s in b.slots:
                 lo = b.start + s.offset
                 view = self.param_buffer[lo:lo + s.numel].view(shapes[s.index])
-                src = init_params[s.index].detach().to(dev)
-                view.copy_(src.to(_BF16))
+                view.copy_(init_params[s.index].detach().to(dev).to(_BF16))
                 self.params[s.index] = view
-                if master_full is not None:
-                    master_full[lo:lo + s.numel].copy_(src.reshape(-1).float())
-        if master_full is not None:
-            self.master.copy_(master_full)
-            del master_full
-        else:
-            for b, off in zip(L.buckets, self._shard_off):
-                lo, hi = b.shard_range(self.shard_index, self.dp)
-                seg = torch.zeros(hi - lo, dtype=torch.float32, device=dev)
-                for s in b.slots:
-                    a, e = b.start + s.offset, b.start + s.offset + s.numel
-                    x0, x1 = max(a, lo), min(e, hi)
-                    if x0 < x1:
-                        seg[x0 - lo:x1 - lo] = init_params[s.index].detach().reshape(-1)[x0 - a:x1 - a].to(dev).float()
-                self.master[off:off + (hi - lo)].copy_(seg)
+        fill_master_shards(L, init_params, self.shard_index, self.master)
 
         # streams / events (one set per bucket, reused every step)
         self.s_pack = torch.cuda.Stream(device=dev)

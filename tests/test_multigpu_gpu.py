@@ -1,0 +1,119 @@
+"""Multi-GPU parity of the DistributedOptimizer (d = 2/4/8), checked on rank 0's
+host against the oracle.  Launches tests/mp_worker.py under torch.distributed.run.
+Skipped when the box has fewer GPUs than the case needs."""
+
+import json
+import random
+import subprocess
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
+from paper_2312_03549_b200.synthetic import make_grads  # noqa: E402
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def _ngpus():
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def u16(t):
+    return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _ulp_bf16(x):
+    x = np.maximum(np.abs(x), np.finfo(np.float32).tiny)
+    return np.exp2(np.floor(np.log2(x)) - 7)
+
+
+def run_workers(tmp_path, n, **kw):
+    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+            str(ROOT / "tests" / "mp_worker.py"), "--out", str(tmp_path)]
+    for k, v in kw.items():
+        args += [f"--{k.replace('_', '-')}", str(v)]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+def check(oracle, tmp_path, n, config, grad_dtype, steps, clip, exact_rs, lr=1e-4,
+          betas=(0.9, 0.95), eps=1e-8, wd=0.1):
+    layouts = [json.loads((tmp_path / f"layout_r{r}.json").read_text()) for r in range(n)]
+    assert all(L == layouts[0] for L in layouts)
+    L = layouts[0]
+    gs = config_gradset(config)
+    gdt = torch.float32 if grad_dtype == "f32" else torch.bfloat16
+    numels = gs.numels
+    for step in range(1, steps + 1):
+        dumps = [np.load(tmp_path / f"r{r}_s{step}.npz") for r in range(n)]
+        # all-gather: every rank holds the same full params
+        for r in range(1, n):
+            np.testing.assert_array_equal(dumps[r]["params"], dumps[0]["params"])
+        grads = [[(g.cpu().numpy() if gdt == torch.float32 else u16(g)).reshape(-1)
+                  for g in make_grads(gs, step, q, "cuda:0", dtype=gdt)] for q in range(n)]
+        shard_base = 0
+        red_all = {r: [] for r in range(n)}
+        for b in L["buckets"]:
+            idx, offs = b["params"], b["offsets"]
+            packs = [oracle.pack([grads[q][i] for i in idx], offs, b["numel"], 1.0 / n) for q in range(n)]
+            sh = b["numel"] // n
+            for r in range(n):
+                dev_red = dumps[r]["reduced"][shard_base:shard_base + sh]
+                red_all[r].append(dev_red)
+                if exact_rs:
+                    np.testing.assert_array_equal(dev_red, oracle.reduce_scatter(packs, r, n))
+                else:
+                    f64 = oracle.reduce_scatter_f64(packs, r, n)
+                    absum = sum(np.abs(oracle.bf16_to_f32(p[r * sh:(r + 1) * sh]).astype(np.float64))
+                                for p in packs)
+                    err = np.abs(oracle.bf16_to_f32(dev_red).astype(np.float64) - f64)
+                    assert np.all(err <= n * 0.5 * _ulp_bf16(absum) + 1e-30), float(err.max())
+            shard_base += sh
+        if clip:
+            ss = sum(oracle.sumsq_bf16(x) for r in range(n) for x in red_all[r])
+            for r in range(n):
+                assert abs(float(dumps[r]["norm"]) - np.sqrt(ss)) <= 1e-5 * np.sqrt(ss)
+                assert dumps[r]["coef"] == dumps[0]["coef"]
+        # AdamW: oracle fed with the device's reduced shard is bit-exact
+        for r in range(n):
+            d = dumps[r]
+            master, m, v = d["pre_master"].copy(), d["pre_m"].copy(), d["pre_v"].copy()
+            coef = float(d["coef"]) if clip else None
+            p_bf16 = oracle.adamw(master, m, v, d["reduced"], step, lr, betas, eps, wd, coef=coef)
+            np.testing.assert_array_equal(master.view(np.uint32), d["master"].view(np.uint32))
+            np.testing.assert_array_equal(m.view(np.uint32), d["m"].view(np.uint32))
+            np.testing.assert_array_equal(v.view(np.uint32), d["v"].view(np.uint32))
+            # the owner's bf16 shard landed in every rank's param buffer
+            base = 0
+            for b in L["buckets"]:
+                sh = b["numel"] // n
+                lo = b["start"] + r * sh
+                np.testing.assert_array_equal(d["params"][lo:lo + sh] if r == 0 else dumps[0]["params"][lo:lo + sh],
+                                              p_bf16[base:base + sh])
+                base += sh
+    del numels
+
+
+CASES = [
+    # (n, config, grad dtype, bucket, clip, backend)
+    (2, "toy", "f32", 4_000_000, 0.0, "nccl"),     # BASELINE config 1: toy GPT, fp32 grads, DP=2
+    (2, "odd", "bf16", 300_000, 0.05, "nccl"),
+    (4, "toy", "bf16", 3_000_000, 1.0, "nccl"),
+    (8, "toy", "bf16", 2_000_000, 0.0, "nccl"),
+]
+
+
+@pytest.mark.parametrize("n,config,gd,bucket,clip,backend", CASES)
+def test_multi_rank_parity(oracle, tmp_path, n, config, gd, bucket, clip, backend):
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs, have {_ngpus()}")
+    run_workers(tmp_path, n, config=config, grad_dtype=gd, bucket=bucket, clip=clip, steps=2,
+                backend=backend)
+    check(oracle, tmp_path, n, config, gd, 2, clip > 0, exact_rs=(backend != "nccl" or n == 2))
