@@ -134,6 +134,59 @@ int hod_all_gather_bf16(const void* send, void* recv, size_t sendcount, void* co
                         void* stream);
 int hod_all_reduce_f32(float* buf, size_t n, void* comm, void* stream);
 
+/* ---- Fused collectives over NVLink peer memory (the B200-native path) ------
+ * The DP row's gradient-bucket and param buffers are symmetric allocations:
+ * every rank maps every peer's buffer (p2p) and an NVLS multicast range
+ * (nvls).  Per bucket one kernel does cross-GPU arrival barrier +
+ * reduce-scatter + AdamW + all-gather (HOD_P2P_FUSED); with clipping the RS
+ * half (HOD_P2P_RS, writes reduced_out + sum-of-squares partials) and the
+ * update half (HOD_P2P_ADAMW_AG, reads reduced_out, scales by *clip_coef) run
+ * on either side of hod_p2p_norm.  Replaces what the reference prices as
+ * reduce_scatter + all_gather (simulator.py:81-89, 327-333) and places after
+ * the flush (simulator.py:445-452), overlapped per bucket instead.
+ * p2p: fp32 rank-order sum, one bf16 rounding (bit-exact vs the oracle).
+ * nvls: multimem.ld_reduce.add.acc::f32 + multimem.st (switch-side reduce and
+ * replicate; one bf16 rounding, switch summation order). */
+#define HOD_P2P_MAX_RANKS 8
+#define HOD_P2P_FUSED 0
+#define HOD_P2P_RS 1
+#define HOD_P2P_ADAMW_AG 2
+
+typedef struct hod_p2p_bucket {
+  uint16_t* grad[HOD_P2P_MAX_RANKS];  /* rank q's bucket base; nvls: [0] = multicast base */
+  uint16_t* param[HOD_P2P_MAX_RANKS]; /* rank q's param-bucket base; nvls: [0] = multicast */
+  uint32_t* flags[HOD_P2P_MAX_RANKS]; /* rank q's flag array: [slot][HOD_P2P_MAX_RANKS] u32 */
+  float* master;                      /* this rank's shard state, n elements each */
+  float* exp_avg;
+  float* exp_avg_sq;
+  uint16_t* reduced_out;  /* local bf16 reduced shard (RS: out, ADAMW_AG: in; FUSED: optional) */
+  float* partials;        /* RS: HOD_SUMSQ_PARTIALS sums of squares (optional) */
+  const float* clip_coef; /* ADAMW_AG: device clip coefficient (optional) */
+  uint32_t* err;          /* device error word (HOD_ETIMEOUT on a barrier timeout) */
+  int64_t shard_off;      /* element offset of this rank's shard inside the bucket */
+  int64_t n;              /* shard elements, multiple of 8 */
+  int d;
+  int rank;
+  int nvls;
+  int slot;               /* barrier slot (bucket index) */
+  uint32_t epoch;         /* monotonically increasing per step, > 0 */
+  unsigned long long timeout_ns; /* barrier spin budget (0 = 20 s) */
+} hod_p2p_bucket;
+
+int hod_p2p_step(const hod_p2p_bucket* bucket, int mode, const hod_adamw_params* hp, void* stream);
+
+/* stand-alone cross-GPU barrier on `slot` (1 CTA): signal then wait for all d ranks */
+int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+                    unsigned long long timeout_ns, uint32_t* err, void* stream);
+
+/* global norm over d ranks through peer memory: fixed-order sum of this rank's
+ * partials, publish to xchg[q][rank] (fp64) of every rank, barrier, rank-order
+ * sum => identical deterministic coef/norm on all ranks. */
+int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg,
+                 uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+                 unsigned long long timeout_ns, uint32_t* err, float max_norm, float* coef,
+                 float* norm, float* sumsq, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

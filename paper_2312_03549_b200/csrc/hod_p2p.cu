@@ -1,0 +1,401 @@
+// hod_p2p.cu — the B200-native collectives of the optimizer step, fused with
+// the update, over NVLink 5 / NVSwitch peer memory.
+//
+// The gradient-bucket buffer and the param buffer of every rank of a DP row
+// are symmetric allocations (one virtual range per rank, mapped into every
+// peer; plus an NVLS multicast range).  Per bucket, after each rank packed
+// its gradients (K1):
+//
+//   fused_rs_adamw_ag  (no clip):   ONE kernel per bucket —
+//       cross-GPU arrival barrier (peer flag stores, acquire spin);
+//       reduce-scatter: rank r sums shard r of every peer's bucket
+//         p2p : d P2P 16-byte loads, fp32 sum in rank order 0..d-1, one RNE
+//               rounding to bf16  -> bit-exact with oracle_rs_sum;
+//         nvls: one multimem.ld_reduce.add.acc::f32 per 8 elements (the
+//               switch reduces; ingress per GPU drops from 2P(d-1)/d to 2P/d);
+//       AdamW on the fp32 master/m/v shard (local HBM, 24 B/elem);
+//       all-gather: the bf16 param vector is stored to every peer's param
+//         bucket (p2p: d stores) or once to the multicast range (nvls:
+//         multimem.st, the switch replicates).
+//   rs (+sumsq partials) / adamw_ag  (clip): the same halves as two kernels,
+//       with the global norm exchanged over peer memory in between.
+//
+// Barriers are monotonic epoch flags: rank r writes `epoch` into slot
+// [slot][r] of every peer's flag array (st.release.sys) and waits until its own
+// [slot][q] >= epoch for all q (ld.acquire.sys).  Every CTA signals (idempotent
+// store), so progress never depends on which CTAs are resident.  Spins are
+// bounded by a %globaltimer budget; on timeout the kernel records HOD_ETIMEOUT
+// in the caller's device error word and skips its work instead of hanging.
+#include <stdint.h>
+#include <string.h>
+
+#include "hod_common.cuh"
+
+namespace hod {
+
+constexpr int kMaxRanks = HOD_P2P_MAX_RANKS;
+
+struct PeerTable {
+  uintptr_t p[kMaxRanks];
+};
+
+struct BarrierArgs {
+  PeerTable flags;          // flags[q] = base of rank q's flag array (device ptrs)
+  uint32_t* local_flags;    // this rank's flag array
+  uint32_t* err;            // device error word (nullable)
+  int slot;
+  uint32_t epoch;
+  unsigned long long timeout_ns;
+};
+
+struct FusedArgs {
+  PeerTable grad;           // p2p: rank q's grad bucket base; nvls: grad[0] = multicast base
+  PeerTable param;          // same for the param bucket
+  const uint16_t* local_grad;  // this rank's bucket base (for the own-shard read)
+  float* master;
+  float* m;
+  float* v;
+  uint16_t* reduced_out;    // optional: local bf16 copy of the reduced shard
+  float* partials;          // optional: HOD_SUMSQ_PARTIALS per-CTA sums of squares
+  const float* coef;        // optional clip coefficient (device)
+  int64_t shard_off;        // element offset of this rank's shard in the bucket
+  int64_t n;                // shard elements (multiple of 8)
+  int d;
+  int rank;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Signal arrival at `slot` to every rank and wait for all of them.  Returns
+// false (and records the error) on timeout.  Must be called by all threads.
+__device__ bool cross_gpu_barrier(const BarrierArgs& b, int d, int rank) {
+  __shared__ int timed_out;
+  if (threadIdx.x == 0) timed_out = 0;
+  __syncthreads();
+  if (threadIdx.x < d) {
+    const int q = threadIdx.x;
+    uint32_t* peer = reinterpret_cast<uint32_t*>(b.flags.p[q]) + b.slot * kMaxRanks + rank;
+    st_release_sys(peer, b.epoch);
+    const uint32_t* mine = b.local_flags + b.slot * kMaxRanks + q;
+    const unsigned long long t0 = globaltimer();
+    while (static_cast<int32_t>(ld_acquire_sys(mine) - b.epoch) < 0) {
+      if (globaltimer() - t0 > b.timeout_ns) {
+        atomicExch(&timed_out, 1);
+        if (b.err) atomicExch(b.err, static_cast<uint32_t>(HOD_ETIMEOUT));
+        break;
+      }
+      __nanosleep(100);
+    }
+  }
+  __syncthreads();
+  return timed_out == 0;
+}
+
+__device__ __forceinline__ uint4 ld_reduce_bf16x8(const uint16_t* mc) {
+  uint4 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(mc)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void st_multicast16(uint16_t* mc, const uint4& q) {
+  // .v4 multimem stores take a float vector; the 16 bytes are moved bit-for-bit
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
+               "f"(__uint_as_float(q.x)), "f"(__uint_as_float(q.y)), "f"(__uint_as_float(q.z)),
+               "f"(__uint_as_float(q.w))
+               : "memory");
+}
+
+// Reduced (bf16-rounded) gradient of 8 elements at bucket element `e`.
+template <int D, bool kNVLS>
+__device__ __forceinline__ void reduce8(const FusedArgs& a, int d, int64_t e, float (&g)[8]) {
+  if constexpr (kNVLS) {
+    unpack8(ld_reduce_bf16x8(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e), g);
+  } else {
+    const int dd = D > 0 ? D : d;
+    uint4 x[D > 0 ? D : kMaxRanks];
+#pragma unroll
+    for (int q = 0; q < (D > 0 ? D : kMaxRanks); ++q)
+      if (q < dd) x[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < (D > 0 ? D : kMaxRanks); ++q) {
+      if (q < dd) {
+        float f[8];
+        unpack8(x[q], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g[k] = bf16_to_f32(f32_to_bf16(acc[k]));
+  }
+}
+
+template <int D, bool kNVLS>
+__device__ __forceinline__ void gather_store8(const FusedArgs& a, int d, int64_t e, const uint4& q8) {
+  if constexpr (kNVLS) {
+    st_multicast16(reinterpret_cast<uint16_t*>(a.param.p[0]) + e, q8);
+  } else {
+    const int dd = D > 0 ? D : d;
+#pragma unroll
+    for (int q = 0; q < (D > 0 ? D : kMaxRanks); ++q)
+      if (q < dd) *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.param.p[q]) + e) = q8;
+  }
+}
+
+__device__ __forceinline__ float block_sum_f(float x) {
+  __shared__ float part[kThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = x;
+  __syncthreads();
+  float s = 0.0f;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kThreads / 32; ++w) s += part[w];
+  return s;
+}
+
+// kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+reduced_out/partials), 2 = AdamW+AG from reduced_out
+template <int D, bool kNVLS, int kMode>
+__global__ void __launch_bounds__(kThreads) p2p_step_kernel(const FusedArgs a, const BarrierArgs b,
+                                                             const AdamWConsts c) {
+  if (kMode != 2) {
+    if (!cross_gpu_barrier(b, a.d, a.rank)) return;
+  }
+  const float coef = (kMode == 2 && a.coef) ? __ldg(a.coef) : 1.0f;
+  const int64_t n_vec = a.n >> 3;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  float ss = 0.0f;
+  for (int64_t iv = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; iv < n_vec; iv += stride) {
+    const int64_t e = a.shard_off + iv * 8;  // element offset inside the bucket
+    float g[8];
+    if (kMode == 2) {
+      unpack8(reinterpret_cast<const uint4*>(a.reduced_out)[iv], g);
+    } else {
+      reduce8<D, kNVLS>(a, a.d, e, g);
+      if (a.reduced_out) reinterpret_cast<uint4*>(a.reduced_out)[iv] = pack8(g);
+      if (kMode == 1) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) ss = __fadd_rn(ss, __fmul_rn(g[k], g[k]));
+        continue;
+      }
+    }
+    float4* p4 = reinterpret_cast<float4*>(a.master) + 2 * iv;
+    float4* m4 = reinterpret_cast<float4*>(a.m) + 2 * iv;
+    float4* v4 = reinterpret_cast<float4*>(a.v) + 2 * iv;
+    const float4 pa = p4[0], pb = p4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+    float pf[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+    float mf[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+    float vf[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const float gk = (kMode == 2 && a.coef) ? __fmul_rn(g[k], coef) : g[k];
+      adamw_elem(pf[k], mf[k], vf[k], gk, c);
+    }
+    p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
+    p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
+    m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
+    m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
+    v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
+    v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
+    gather_store8<D, kNVLS>(a, a.d, e, pack8(pf));
+  }
+  if (kMode == 1 && a.partials) {
+    const float s = block_sum_f(ss);
+    if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
+  }
+  if (kMode != 1) __threadfence_system();  // remote param stores performed before any later signal
+}
+
+__global__ void barrier_kernel(const BarrierArgs b, int d, int rank) {
+  __threadfence_system();
+  cross_gpu_barrier(b, d, rank);
+}
+
+// Global-norm exchange: every rank publishes its fp64 partial sum of squares
+// into slot `rank` of every peer's exchange array, then (after the barrier)
+// sums all d slots in rank order -> identical, deterministic norm everywhere.
+__global__ void norm_exchange_kernel(const float* partials, int64_t n_partials, PeerTable xchg,
+                                     double* local_xchg, const BarrierArgs b, int d, int rank,
+                                     float max_norm, float* coef, float* norm, float* sumsq_out) {
+  __shared__ double mine;
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int64_t i = 0; i < n_partials; ++i) s += static_cast<double>(partials[i]);
+    mine = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < d) {
+    double* dst = reinterpret_cast<double*>(xchg.p[threadIdx.x]) + rank;
+    *reinterpret_cast<volatile double*>(dst) = mine;
+  }
+  __threadfence_system();
+  __syncthreads();
+  if (!cross_gpu_barrier(b, d, rank)) return;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < d; ++q) t += *reinterpret_cast<volatile double*>(local_xchg + q);
+    const float s32 = static_cast<float>(t);
+    const float nrm = __fsqrt_rn(s32);
+    const float cf = __fdiv_rn(max_norm, __fadd_rn(nrm, 1e-6f));
+    *coef = cf < 1.0f ? cf : 1.0f;
+    if (norm) *norm = nrm;
+    if (sumsq_out) *sumsq_out = s32;
+  }
+}
+
+template <int D, bool kNVLS, int kMode>
+static void launch_step(const FusedArgs& a, const BarrierArgs& b, const AdamWConsts& c, int grid,
+                        cudaStream_t s) {
+  count_launch(1);
+  p2p_step_kernel<D, kNVLS, kMode><<<grid, kThreads, 0, s>>>(a, b, c);
+}
+
+template <bool kNVLS, int kMode>
+static void dispatch_d(const FusedArgs& a, const BarrierArgs& b, const AdamWConsts& c, int grid,
+                       cudaStream_t s) {
+  switch (kNVLS ? 0 : a.d) {
+    case 2: launch_step<2, kNVLS, kMode>(a, b, c, grid, s); break;
+    case 4: launch_step<4, kNVLS, kMode>(a, b, c, grid, s); break;
+    case 8: launch_step<8, kNVLS, kMode>(a, b, c, grid, s); break;
+    default: launch_step<0, kNVLS, kMode>(a, b, c, grid, s); break;
+  }
+}
+
+static int fill_tables(const hod_p2p_bucket* bk, FusedArgs* a, BarrierArgs* b) {
+  if (!bk || bk->d < 1 || bk->d > kMaxRanks || bk->rank < 0 || bk->rank >= bk->d) {
+    set_error("hod_p2p: bad group (d=%d rank=%d)", bk ? bk->d : -1, bk ? bk->rank : -1);
+    return HOD_EINVAL;
+  }
+  if (bk->n < 0 || (bk->n & 7) != 0 || (bk->shard_off & 7) != 0) {
+    set_error("hod_p2p: shard size/offset must be multiples of 8 elements");
+    return HOD_EALIGN;
+  }
+  memset(a, 0, sizeof(*a));
+  memset(b, 0, sizeof(*b));
+  const int nptr = bk->nvls ? 1 : bk->d;
+  for (int q = 0; q < nptr; ++q) {
+    a->grad.p[q] = reinterpret_cast<uintptr_t>(bk->grad[q]);
+    a->param.p[q] = reinterpret_cast<uintptr_t>(bk->param[q]);
+    if (!a->grad.p[q] || !a->param.p[q] || (a->grad.p[q] & 15) || (a->param.p[q] & 15)) {
+      set_error("hod_p2p: peer buffer %d null or not 16-byte aligned", q);
+      return HOD_EALIGN;
+    }
+  }
+  for (int q = 0; q < bk->d; ++q) {
+    b->flags.p[q] = reinterpret_cast<uintptr_t>(bk->flags[q]);
+    if (!b->flags.p[q]) { set_error("hod_p2p: null flag array %d", q); return HOD_EINVAL; }
+  }
+  b->local_flags = bk->flags[bk->rank];
+  b->err = bk->err;
+  b->slot = bk->slot;
+  b->epoch = bk->epoch;
+  b->timeout_ns = bk->timeout_ns ? bk->timeout_ns : 20000000000ull;
+  a->master = bk->master;
+  a->m = bk->exp_avg;
+  a->v = bk->exp_avg_sq;
+  a->reduced_out = bk->reduced_out;
+  a->partials = bk->partials;
+  a->coef = bk->clip_coef;
+  a->shard_off = bk->shard_off;
+  a->n = bk->n;
+  a->d = bk->d;
+  a->rank = bk->rank;
+  return HOD_OK;
+}
+
+}  // namespace hod
+
+using namespace hod;
+
+extern "C" {
+
+int hod_p2p_step(const hod_p2p_bucket* bk, int mode, const hod_adamw_params* hp, void* stream) {
+  FusedArgs a;
+  BarrierArgs b;
+  int rc = fill_tables(bk, &a, &b);
+  if (rc) return rc;
+  if (mode < HOD_P2P_FUSED || mode > HOD_P2P_ADAMW_AG) { set_error("hod_p2p_step: bad mode %d", mode); return HOD_EINVAL; }
+  if (mode != HOD_P2P_RS && (!hp || hp->step < 1)) { set_error("hod_p2p_step: bad hp/step"); return HOD_EINVAL; }
+  if (mode != HOD_P2P_RS && (!a.master || !a.m || !a.v)) { set_error("hod_p2p_step: null state"); return HOD_EINVAL; }
+  if (mode == HOD_P2P_ADAMW_AG && !a.reduced_out) { set_error("hod_p2p_step: ADAMW_AG needs reduced_out"); return HOD_EINVAL; }
+  if (mode == HOD_P2P_RS && !a.reduced_out && !a.partials) { set_error("hod_p2p_step: RS writes nothing"); return HOD_EINVAL; }
+  const AdamWConsts c = (mode != HOD_P2P_RS) ? fold_adamw(*hp) : AdamWConsts{};
+  // RS keeps a FIXED grid so its sum-of-squares partials are reproducible
+  const int grid = (mode == HOD_P2P_RS) ? HOD_SUMSQ_PARTIALS : grid_for(a.n / 8, kThreads, 4);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const bool nv = bk->nvls != 0;
+  if (mode == HOD_P2P_FUSED) {
+    if (nv) dispatch_d<true, 0>(a, b, c, grid, s); else dispatch_d<false, 0>(a, b, c, grid, s);
+  } else if (mode == HOD_P2P_RS) {
+    if (nv) dispatch_d<true, 1>(a, b, c, grid, s); else dispatch_d<false, 1>(a, b, c, grid, s);
+  } else {
+    if (nv) dispatch_d<true, 2>(a, b, c, grid, s); else dispatch_d<false, 2>(a, b, c, grid, s);
+  }
+  return cuda_status(cudaGetLastError(), "hod_p2p_step launch");
+}
+
+int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+                    unsigned long long timeout_ns, uint32_t* err, void* stream) {
+  if (!flags || d < 1 || d > kMaxRanks || rank < 0 || rank >= d || slot < 0) {
+    set_error("hod_p2p_barrier: bad arguments"); return HOD_EINVAL;
+  }
+  BarrierArgs b;
+  memset(&b, 0, sizeof(b));
+  for (int q = 0; q < d; ++q) b.flags.p[q] = reinterpret_cast<uintptr_t>(flags[q]);
+  b.local_flags = flags[rank];
+  b.err = err;
+  b.slot = slot;
+  b.epoch = epoch;
+  b.timeout_ns = timeout_ns ? timeout_ns : 20000000000ull;
+  count_launch(1);
+  barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(b, d, rank);
+  return cuda_status(cudaGetLastError(), "hod_p2p_barrier launch");
+}
+
+int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg, uint32_t* const* flags,
+                 int d, int rank, int slot, uint32_t epoch, unsigned long long timeout_ns, uint32_t* err,
+                 float max_norm, float* coef, float* norm, float* sumsq, void* stream) {
+  if (!partials || !xchg || !flags || !coef || d < 1 || d > kMaxRanks || rank < 0 || rank >= d ||
+      !(max_norm > 0.0f)) {
+    set_error("hod_p2p_norm: bad arguments"); return HOD_EINVAL;
+  }
+  PeerTable x;
+  memset(&x, 0, sizeof(x));
+  BarrierArgs b;
+  memset(&b, 0, sizeof(b));
+  for (int q = 0; q < d; ++q) {
+    x.p[q] = reinterpret_cast<uintptr_t>(xchg[q]);
+    b.flags.p[q] = reinterpret_cast<uintptr_t>(flags[q]);
+  }
+  b.local_flags = flags[rank];
+  b.err = err;
+  b.slot = slot;
+  b.epoch = epoch;
+  b.timeout_ns = timeout_ns ? timeout_ns : 20000000000ull;
+  count_launch(1);
+  norm_exchange_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      partials, n_partials, x, xchg[rank], b, d, rank, max_norm, coef, norm, sumsq);
+  return cuda_status(cudaGetLastError(), "hod_p2p_norm launch");
+}
+
+}  // extern "C"

@@ -17,8 +17,14 @@ plus all-gather of the stage's gradient bytes charged after the pipeline
 flush (simulator.py:327-333, 445-452) — with the real,
 overlapped operation.  The ``backend`` selects how C1/C2 move bytes:
 
-* ``"nccl"`` — NCCL ReduceScatter / AllGather (bf16, sum) over NVLink; the
-  library baseline.
+* ``"p2p"`` (default for d > 1) — our fused kernels over NVLink peer memory:
+  one kernel per bucket does the cross-GPU arrival barrier, the
+  reduce-scatter (P2P loads, fp32 rank-order sum: deterministic and bit-exact
+  with the oracle), the AdamW update and the all-gather (P2P stores).
+* ``"nvls"`` — the same fused kernel with NVSwitch in-switch reduction
+  (multimem.ld_reduce) and multicast stores (multimem.st).
+* ``"nccl"`` — NCCL ReduceScatter / AllGather (bf16, sum) around our K2; the
+  library baseline the fused path is measured against.
 * ``"none"`` — d == 1: no collective, AdamW reads the packed bucket.
 """
 
@@ -36,6 +42,7 @@ from .comm import DPGroup, NcclComm
 from .errors import InfeasibleConfigError
 
 _BF16 = torch.bfloat16
+BACKENDS = ("none", "nccl", "p2p", "nvls")
 
 
 @dataclass
@@ -112,7 +119,8 @@ class DistributedOptimizer:
                  weight_decay: float = 0.1, clip: float | None = None,
                  bucket_size: int = 25_000_000, dp_group: DPGroup | None = None,
                  norm_ranks=None, grad_scale: float | None = None, backend: str = "auto",
-                 device=None, param_align: int = 64):
+                 device=None, param_align: int = 64, process_group=None, norm_group=None,
+                 keep_reduced: bool = False, barrier_timeout_s: float = 20.0):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -124,12 +132,16 @@ class DistributedOptimizer:
         self.shard_index = self.group.index
         self.grad_scale = (1.0 / self.dp) if grad_scale is None else float(grad_scale)
         if backend == "auto":
-            backend = "none" if self.dp == 1 else "nccl"
-        if backend not in ("none", "nccl"):
-            raise InfeasibleConfigError(f"unknown backend {backend!r}")
-        if backend == "none" and self.dp != 1:
-            raise InfeasibleConfigError("backend 'none' needs a single-rank DP group")
+            backend = "none" if self.dp == 1 else "p2p"
+        if backend not in BACKENDS:
+            raise InfeasibleConfigError(f"unknown backend {backend!r} (choose from {BACKENDS})")
+        if (backend == "none") != (self.dp == 1):
+            raise InfeasibleConfigError(f"backend {backend!r} does not fit a DP row of {self.dp}")
+        if backend in ("p2p", "nvls") and self.dp > nat.HOD_P2P_MAX_RANKS:
+            raise InfeasibleConfigError(f"{backend} supports at most {nat.HOD_P2P_MAX_RANKS} ranks")
         self.backend = backend
+        self.keep_reduced = keep_reduced
+        self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
 
         shapes = [tuple(p.shape) for p in init_params]
@@ -138,8 +150,29 @@ class DistributedOptimizer:
         L = self.layout
         total = L.total_numel
         dev = self.device
-        self.param_buffer = torch.zeros(total, dtype=_BF16, device=dev)
-        self.grad_buffer = torch.empty(total, dtype=_BF16, device=dev)
+        nb = len(L.buckets)
+        self._sym = None
+        if backend in ("p2p", "nvls"):
+            from .symm import SymmetricTensor, group_for
+
+            pg = process_group if process_group is not None else group_for(self.group.ranks)
+            self._pg = pg
+            self._sym_grad = SymmetricTensor(total, _BF16, dev, pg)
+            self._sym_param = SymmetricTensor(total, _BF16, dev, pg, zero=True)
+            # barrier flags: slots 0..nb-1 per bucket, nb = end-of-step
+            self._sym_flags = SymmetricTensor((nb + 1) * nat.HOD_P2P_MAX_RANKS, torch.int32, dev, pg,
+                                              zero=True)
+            if self._sym_grad.rank != self.shard_index:
+                raise InfeasibleConfigError("process group order differs from the DP row order")
+            if backend == "nvls" and not (self._sym_grad.mc and self._sym_param.mc):
+                raise InfeasibleConfigError("NVLS multicast unavailable; use backend='p2p'")
+            self.param_buffer = self._sym_param.tensor
+            self.grad_buffer = self._sym_grad.tensor
+            self._err = torch.zeros(1, dtype=torch.int32, device=dev)
+            self._norm_group = norm_group
+        else:
+            self.param_buffer = torch.zeros(total, dtype=_BF16, device=dev)
+            self.grad_buffer = torch.empty(total, dtype=_BF16, device=dev)
         shard_total = total // self.dp
         self.master = torch.empty(shard_total, dtype=torch.float32, device=dev)
         self.exp_avg = torch.zeros(shard_total, dtype=torch.float32, device=dev)
@@ -183,8 +216,23 @@ class DistributedOptimizer:
         norm_ranks = tuple(norm_ranks) if norm_ranks is not None else self.group.ranks
         self.norm_ranks = norm_ranks
         if self.clip is not None and len(norm_ranks) > 1:
-            self.norm_comm = (self.comm if norm_ranks == self.group.ranks and self.comm is not None
-                              else NcclComm(norm_ranks, self.group.global_rank, "norm"))
+            if self.backend in ("p2p", "nvls"):
+                from .symm import SymmetricTensor, group_for
+
+                ng = (self._pg if norm_ranks == self.group.ranks
+                      else (self._norm_group if self._norm_group is not None else group_for(norm_ranks)))
+                self._norm_xchg = SymmetricTensor(nat.HOD_P2P_MAX_RANKS, torch.float64, dev, ng, zero=True)
+                self._norm_flags = SymmetricTensor(nat.HOD_P2P_MAX_RANKS, torch.int32, dev, ng, zero=True)
+                self._norm_rank = self._norm_xchg.rank
+                self._norm_d = self._norm_xchg.world
+            else:
+                self.norm_comm = (self.comm if norm_ranks == self.group.ranks and self.comm is not None
+                                  else NcclComm(norm_ranks, self.group.global_rank, "norm"))
+        if self.backend in ("p2p", "nvls"):
+            torch.cuda.synchronize(dev)
+            import torch.distributed as dist
+
+            dist.barrier()  # every rank's zeroed flags exist before anyone signals
 
         self._ktiming = None
         self._staging = None
@@ -226,7 +274,9 @@ class DistributedOptimizer:
             if not self._launched[b]:
                 missing = [s.index for s in L.buckets[b].slots if s.index not in self._pending_grads[b]]
                 raise InfeasibleConfigError(f"bucket {b} is missing gradients for params {missing[:8]}")
-        if self.clip is not None:
+        if self.backend in ("p2p", "nvls"):
+            self._p2p_finish()
+        elif self.clip is not None:
             self._clip_and_update()
         else:
             self._flush_deferred_ag()
@@ -334,6 +384,16 @@ class DistributedOptimizer:
         self._ev_packed[bi].record(self.s_pack)
         self._launched[bi] = True
 
+        if self.backend in ("p2p", "nvls"):
+            self.s_comm.wait_event(self._ev_packed[bi])
+            shard_ptr, _ = self._grad_shard(b)
+            if self.clip is None:
+                self._p2p(bi, nat.HOD_P2P_FUSED, reduced_out=shard_ptr if self.keep_reduced else None)
+            else:
+                part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * bi
+                self._p2p(bi, nat.HOD_P2P_RS, reduced_out=shard_ptr, partials=part)
+            return
+
         reduced = self._ev_packed[bi]
         if self.backend == "nccl":
             self.s_comm.wait_event(self._ev_packed[bi])
@@ -380,6 +440,82 @@ class DistributedOptimizer:
     def _flush_deferred_ag(self, keep_last: bool = False) -> None:
         while len(self._deferred_ag) > (1 if keep_last else 0):
             self._issue_ag(self._deferred_ag.pop(0))
+
+    # ------------------------------------------------- fused peer-memory path
+    def _flag_ptrs(self, sym) -> ctypes.Array:
+        arr = (ctypes.c_void_p * sym.world)()
+        for q in range(sym.world):
+            arr[q] = sym.peer(q)
+        return arr
+
+    def _p2p(self, bi: int, mode: int, reduced_out=None, partials=None, coef_ptr=None) -> None:
+        b = self.layout.buckets[bi]
+        d, n = self.dp, b.numel // self.dp
+        off = self._shard_off[bi]
+        bk = nat.P2PBucket()
+        if self.backend == "nvls":
+            bk.grad[0] = self._sym_grad.multicast(2 * b.start)
+            bk.param[0] = self._sym_param.multicast(2 * b.start)
+        else:
+            for q in range(d):
+                bk.grad[q] = self._sym_grad.peer(q, 2 * b.start)
+                bk.param[q] = self._sym_param.peer(q, 2 * b.start)
+        for q in range(d):
+            bk.flags[q] = self._sym_flags.peer(q)
+        bk.master = _ptr(self.master) + 4 * off
+        bk.exp_avg = _ptr(self.exp_avg) + 4 * off
+        bk.exp_avg_sq = _ptr(self.exp_avg_sq) + 4 * off
+        bk.reduced_out = reduced_out
+        bk.partials = partials
+        bk.clip_coef = coef_ptr
+        bk.err = _ptr(self._err)
+        bk.shard_off = self.shard_index * n
+        bk.n = n
+        bk.d, bk.rank, bk.nvls = d, self.shard_index, int(self.backend == "nvls")
+        bk.slot, bk.epoch, bk.timeout_ns = bi, self.step_count, self.timeout_ns
+        hp = self._hp()
+        name = {nat.HOD_P2P_FUSED: "fused", nat.HOD_P2P_RS: "rs", nat.HOD_P2P_ADAMW_AG: "adamw_ag"}[mode]
+        # algorithmic bytes per launch: local HBM (state 24 B + own param 2 B +
+        # own grad 2 B per owned element) — NVLink bytes are reported separately
+        nbytes = {"fused": 28 * n, "rs": 2 * d * n + 2 * n, "adamw_ag": 28 * n}[name]
+        t0 = self._timed_event(self.s_comm)
+        nat.call("hod_p2p_step", ctypes.byref(bk), mode, ctypes.byref(hp), nat.stream_ptr(self.s_comm))
+        self._timed_close(name, t0, self.s_comm, nbytes)
+
+    def _p2p_finish(self) -> None:
+        nb = len(self.layout.buckets)
+        s = self.s_comm
+        if self.clip is not None:
+            if self.norm_ranks == (self.group.global_rank,) or len(self.norm_ranks) == 1:
+                nat.call("hod_sum_partials", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS,
+                         _ptr(self._sumsq), nat.stream_ptr(s))
+                nat.call("hod_clip_coef", _ptr(self._sumsq), ctypes.c_float(self.clip),
+                         _ptr(self._coef), _ptr(self._norm), nat.stream_ptr(s))
+            else:
+                xchg = self._flag_ptrs(self._norm_xchg)
+                flags = self._flag_ptrs(self._norm_flags)
+                nat.call("hod_p2p_norm", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS, xchg, flags,
+                         self._norm_d, self._norm_rank, 0, self.step_count, self.timeout_ns,
+                         _ptr(self._err), ctypes.c_float(self.clip), _ptr(self._coef), _ptr(self._norm),
+                         _ptr(self._sumsq), nat.stream_ptr(s))
+            for bi, b in enumerate(self.layout.buckets):
+                shard_ptr, _ = self._grad_shard(b)
+                self._p2p(bi, nat.HOD_P2P_ADAMW_AG, reduced_out=shard_ptr, coef_ptr=_ptr(self._coef))
+        # end-of-step barrier: every rank's param stores (and reads of our
+        # buckets) are complete before anyone uses the params or repacks
+        nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,
+                 self.step_count, self.timeout_ns, _ptr(self._err), nat.stream_ptr(s))
+        for ev in self._ev_params:
+            ev.record(s)
+
+    def check_health(self) -> None:
+        """Raise DeviceError if a cross-GPU barrier timed out (synchronises)."""
+        if getattr(self, "_err", None) is not None:
+            code = int(self._err.item())
+            if code:
+                from .errors import DeviceError
+
+                raise DeviceError(f"fused collective reported error {code} (barrier timeout)")
 
     def _clip_and_update(self) -> None:
         nb = len(self.layout.buckets)

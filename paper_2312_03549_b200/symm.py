@@ -1,0 +1,61 @@
+"""Symmetric (peer-mapped + NVLS multicast) buffers for the fused collectives.
+
+Allocation and the handle exchange are plumbing borrowed from
+``torch.distributed._symmetric_memory`` (cuMem VMM under the hood); all data
+movement on these buffers is done by our own kernels (csrc/hod_p2p.cu).  Each
+rank of the DP row maps every peer's copy (``ptrs[q]``) and, when the box
+supports NVLS, one multicast address (``mc``) whose loads reduce across all
+copies (multimem.ld_reduce) and whose stores land in all of them.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .errors import DeviceError
+
+
+def _symm():
+    import torch.distributed._symmetric_memory as symm_mem
+
+    return symm_mem
+
+
+class SymmetricTensor:
+    """One symmetric allocation over ``group``: the local tensor + peer/mc pointers."""
+
+    def __init__(self, numel: int, dtype: torch.dtype, device, group, zero: bool = False):
+        symm_mem = _symm()
+        self.tensor = symm_mem.empty(numel, dtype=dtype, device=device)
+        if zero:
+            self.tensor.zero_()
+        name = group.group_name if group is not None else dist.group.WORLD.group_name
+        self.handle = symm_mem.rendezvous(self.tensor, name)
+        self.ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        self.mc = int(self.handle.multicast_ptr or 0)
+        self.rank = int(self.handle.rank)
+        self.world = int(self.handle.world_size)
+        if self.ptrs[self.rank] != self.tensor.data_ptr():
+            raise DeviceError("symmetric rendezvous returned an unexpected local pointer")
+
+    def peer(self, q: int, byte_offset: int = 0) -> int:
+        return self.ptrs[q] + byte_offset
+
+    def multicast(self, byte_offset: int = 0) -> int:
+        if not self.mc:
+            raise DeviceError("NVLS multicast is not available on this group/box")
+        return self.mc + byte_offset
+
+
+def group_for(ranks, world_group_ranks=None):
+    """Process group over ``ranks`` (WORLD when it spans everybody).
+
+    ``dist.new_group`` is collective over the WORLD: callers that need several
+    disjoint DP rows (config 4) should build them with
+    ``dist.new_subgroups_by_enumeration`` on every rank instead and pass the
+    row's group explicitly."""
+    ranks = tuple(ranks)
+    if len(ranks) == dist.get_world_size() and sorted(ranks) == list(range(len(ranks))):
+        return dist.group.WORLD
+    return dist.new_group(list(ranks))

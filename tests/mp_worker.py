@@ -54,7 +54,8 @@ def main():
     gdt = torch.float32 if a.grad_dtype == "f32" else torch.bfloat16
     clip = a.clip if a.clip > 0 else None
     opt = DistributedOptimizer(init_params(gs, dev), bucket_size=a.bucket, clip=clip,
-                               dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend)
+                               dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
+                               keep_reduced=True, barrier_timeout_s=30.0)
     L = opt.layout
     out = Path(a.out)
     for step in range(1, a.steps + 1):
@@ -72,6 +73,7 @@ def main():
                  pre_v=pre["v"],
                  coef=np.float32(rep.clip_coef.item()) if rep.clip_coef is not None else np.float32(-1),
                  norm=np.float32(rep.grad_norm.item()) if rep.grad_norm is not None else np.float32(-1))
+    opt.check_health()
     (out / f"layout_r{rank}.json").write_text(L.to_json())
     opt.close()
     dist.barrier()
