@@ -27,6 +27,7 @@
 // bounded by a %globaltimer budget; on timeout the kernel records HOD_ETIMEOUT
 // in the caller's device error word and skips its work instead of hanging.
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "hod_common.cuh"
@@ -122,34 +123,6 @@ __device__ __forceinline__ void st_multicast16(uint16_t* mc, const uint4& q) {
                : "memory");
 }
 
-// Reduced (bf16-rounded) gradient of 8 elements at bucket element `e`.
-template <int D, bool kNVLS>
-__device__ __forceinline__ void reduce8(const FusedArgs& a, int d, int64_t e, float (&g)[8]) {
-  if constexpr (kNVLS) {
-    unpack8(ld_reduce_bf16x8(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e), g);
-  } else {
-    const int dd = D > 0 ? D : d;
-    uint4 x[D > 0 ? D : kMaxRanks];
-#pragma unroll
-    for (int q = 0; q < (D > 0 ? D : kMaxRanks); ++q)
-      if (q < dd) x[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
-    float acc[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
-#pragma unroll
-    for (int q = 0; q < (D > 0 ? D : kMaxRanks); ++q) {
-      if (q < dd) {
-        float f[8];
-        unpack8(x[q], f);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) g[k] = bf16_to_f32(f32_to_bf16(acc[k]));
-  }
-}
-
 template <int D, bool kNVLS>
 __device__ __forceinline__ void gather_store8(const FusedArgs& a, int d, int64_t e, const uint4& q8) {
   if constexpr (kNVLS) {
@@ -174,8 +147,94 @@ __device__ __forceinline__ float block_sum_f(float x) {
   return s;
 }
 
-// kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+reduced_out/partials), 2 = AdamW+AG from reduced_out
+// One thread's 8-element work item, split into a load phase and a compute /
+// store phase so that U items can have all their loads in flight at once.
+template <int D, bool kNVLS>
+struct Item {
+  static constexpr int kRaw = kNVLS ? 1 : (D > 0 ? D : kMaxRanks);
+  uint4 raw[kRaw];     // peers' bucket vectors (p2p), the switch-reduced vector (nvls),
+                       // or the local reduced shard (mode 2, raw[0])
+  float4 st[6];        // master, m, v (two float4 each)
+};
+
 template <int D, bool kNVLS, int kMode>
+__device__ __forceinline__ void load_item(const FusedArgs& a, int64_t iv, Item<D, kNVLS>& it) {
+  const int64_t e = a.shard_off + iv * 8;
+  if (kMode == 2) {
+    it.raw[0] = reinterpret_cast<const uint4*>(a.reduced_out)[iv];
+  } else if constexpr (kNVLS) {
+    it.raw[0] = ld_reduce_bf16x8(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e);
+  } else {
+    const int dd = D > 0 ? D : a.d;
+#pragma unroll
+    for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q)
+      if (q < dd) it.raw[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
+  }
+  if (kMode != 1) {
+    const float4* p4 = reinterpret_cast<const float4*>(a.master) + 2 * iv;
+    const float4* m4 = reinterpret_cast<const float4*>(a.m) + 2 * iv;
+    const float4* v4 = reinterpret_cast<const float4*>(a.v) + 2 * iv;
+    it.st[0] = p4[0]; it.st[1] = p4[1];
+    it.st[2] = m4[0]; it.st[3] = m4[1];
+    it.st[4] = v4[0]; it.st[5] = v4[1];
+  }
+}
+
+template <int D, bool kNVLS, int kMode>
+__device__ __forceinline__ void finish_item(const FusedArgs& a, int64_t iv, const Item<D, kNVLS>& it,
+                                            const AdamWConsts& c, float coef, float& ss) {
+  const int64_t e = a.shard_off + iv * 8;
+  float g[8];
+  if (kMode == 2 || kNVLS) {
+    unpack8(it.raw[0], g);
+  } else {
+    const int dd = D > 0 ? D : a.d;
+    float acc[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+#pragma unroll
+    for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q) {
+      if (q < dd) {
+        float f[8];
+        unpack8(it.raw[q], f);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) g[k] = bf16_to_f32(f32_to_bf16(acc[k]));
+  }
+  if (kMode != 2) {
+    if (a.reduced_out) reinterpret_cast<uint4*>(a.reduced_out)[iv] = pack8(g);
+    if (kMode == 1) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) ss = __fadd_rn(ss, __fmul_rn(g[k], g[k]));
+      return;
+    }
+  }
+  float pf[8] = {it.st[0].x, it.st[0].y, it.st[0].z, it.st[0].w, it.st[1].x, it.st[1].y, it.st[1].z, it.st[1].w};
+  float mf[8] = {it.st[2].x, it.st[2].y, it.st[2].z, it.st[2].w, it.st[3].x, it.st[3].y, it.st[3].z, it.st[3].w};
+  float vf[8] = {it.st[4].x, it.st[4].y, it.st[4].z, it.st[4].w, it.st[5].x, it.st[5].y, it.st[5].z, it.st[5].w};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float gk = (kMode == 2 && a.coef) ? __fmul_rn(g[k], coef) : g[k];
+    adamw_elem(pf[k], mf[k], vf[k], gk, c);
+  }
+  float4* p4 = reinterpret_cast<float4*>(a.master) + 2 * iv;
+  float4* m4 = reinterpret_cast<float4*>(a.m) + 2 * iv;
+  float4* v4 = reinterpret_cast<float4*>(a.v) + 2 * iv;
+  p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
+  p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
+  m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
+  m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
+  v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
+  v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
+  gather_store8<D, kNVLS>(a, a.d, e, pack8(pf));
+}
+
+// kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+reduced_out/partials), 2 = AdamW+AG from reduced_out
+// U: work items per thread in flight (memory-level parallelism for the NVLink loads)
+template <int D, bool kNVLS, int kMode, int U>
 __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const FusedArgs a, const BarrierArgs b,
                                                              const AdamWConsts c) {
   if (kMode != 2) {
@@ -185,39 +244,15 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const FusedArgs a, c
   const int64_t n_vec = a.n >> 3;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   float ss = 0.0f;
-  for (int64_t iv = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; iv < n_vec; iv += stride) {
-    const int64_t e = a.shard_off + iv * 8;  // element offset inside the bucket
-    float g[8];
-    if (kMode == 2) {
-      unpack8(reinterpret_cast<const uint4*>(a.reduced_out)[iv], g);
-    } else {
-      reduce8<D, kNVLS>(a, a.d, e, g);
-      if (a.reduced_out) reinterpret_cast<uint4*>(a.reduced_out)[iv] = pack8(g);
-      if (kMode == 1) {
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; base < n_vec;
+       base += stride * U) {
+    Item<D, kNVLS> it[U];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) ss = __fadd_rn(ss, __fmul_rn(g[k], g[k]));
-        continue;
-      }
-    }
-    float4* p4 = reinterpret_cast<float4*>(a.master) + 2 * iv;
-    float4* m4 = reinterpret_cast<float4*>(a.m) + 2 * iv;
-    float4* v4 = reinterpret_cast<float4*>(a.v) + 2 * iv;
-    const float4 pa = p4[0], pb = p4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
-    float pf[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-    float mf[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-    float vf[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+    for (int u = 0; u < U; ++u)
+      if (base + u * stride < n_vec) load_item<D, kNVLS, kMode>(a, base + u * stride, it[u]);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const float gk = (kMode == 2 && a.coef) ? __fmul_rn(g[k], coef) : g[k];
-      adamw_elem(pf[k], mf[k], vf[k], gk, c);
-    }
-    p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
-    p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
-    m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
-    m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
-    v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
-    v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
-    gather_store8<D, kNVLS>(a, a.d, e, pack8(pf));
+    for (int u = 0; u < U; ++u)
+      if (base + u * stride < n_vec) finish_item<D, kNVLS, kMode>(a, base + u * stride, it[u], c, coef, ss);
   }
   if (kMode == 1 && a.partials) {
     const float s = block_sum_f(ss);
@@ -263,11 +298,25 @@ __global__ void norm_exchange_kernel(const float* partials, int64_t n_partials, 
   }
 }
 
+static int unroll_setting() {
+  static int u = [] {
+    const char* e = getenv("HOD_P2P_UNROLL");
+    return e ? atoi(e) : 0;  // 0 = auto
+  }();
+  return u;
+}
+
 template <int D, bool kNVLS, int kMode>
 static void launch_step(const FusedArgs& a, const BarrierArgs& b, const AdamWConsts& c, int grid,
                         cudaStream_t s) {
   count_launch(1);
-  p2p_step_kernel<D, kNVLS, kMode><<<grid, kThreads, 0, s>>>(a, b, c);
+  // measured (tools/p2p_microbench.py): two items in flight per thread pay off
+  // at d = 2 (one remote load each); at d >= 4 the register cost outweighs it
+  const int u = unroll_setting();
+  if (u >= 2 || (u == 0 && D == 2))
+    p2p_step_kernel<D, kNVLS, kMode, 2><<<grid, kThreads, 0, s>>>(a, b, c);
+  else
+    p2p_step_kernel<D, kNVLS, kMode, 1><<<grid, kThreads, 0, s>>>(a, b, c);
 }
 
 template <bool kNVLS, int kMode>

@@ -131,8 +131,12 @@ class DistributedOptimizer:
         self.dp = self.group.size
         self.shard_index = self.group.index
         self.grad_scale = (1.0 / self.dp) if grad_scale is None else float(grad_scale)
-        if backend == "auto":
-            backend = "none" if self.dp == 1 else "p2p"
+        auto = backend == "auto"
+        if auto:
+            # measured choice (tools/p2p_microbench.py): P2P loads/stores
+            # up to d = 4; at d = 8 NVLS moves 18n instead of 28n bytes per
+            # direction per GPU (falls back to p2p when multicast is unavailable)
+            backend = "none" if self.dp == 1 else ("nvls" if self.dp >= 8 else "p2p")
         if backend not in BACKENDS:
             raise InfeasibleConfigError(f"unknown backend {backend!r} (choose from {BACKENDS})")
         if (backend == "none") != (self.dp == 1):
@@ -165,7 +169,9 @@ class DistributedOptimizer:
             if self._sym_grad.rank != self.shard_index:
                 raise InfeasibleConfigError("process group order differs from the DP row order")
             if backend == "nvls" and not (self._sym_grad.mc and self._sym_param.mc):
-                raise InfeasibleConfigError("NVLS multicast unavailable; use backend='p2p'")
+                if not auto:
+                    raise InfeasibleConfigError("NVLS multicast unavailable; use backend='p2p'")
+                self.backend = backend = "p2p"
             self.param_buffer = self._sym_param.tensor
             self.grad_buffer = self._sym_grad.tensor
             self._err = torch.zeros(1, dtype=torch.int32, device=dev)

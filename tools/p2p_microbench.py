@@ -1,0 +1,136 @@
+"""Micro-benchmark of the fused peer-memory collectives vs NCCL on one bucket.
+
+    torchrun --nproc-per-node N tools/p2p_microbench.py [--numel 100000000]
+
+Per rank, for a bucket of ``numel`` bf16 elements (shard n = numel/N):
+  fused_p2p / fused_nvls : barrier + RS + AdamW + AG in one kernel
+  rs_p2p / rs_nvls       : barrier + RS only (reduced shard + sumsq partials)
+  adamw_ag_p2p / _nvls   : AdamW + AG from the local reduced shard
+  nccl_rs+ag             : ncclReduceScatter + ncclAllGather (bf16, in place)
+  adamw_local            : K2 on the shard (HBM only)
+Times are CUDA-event device times (max over ranks), after warm-up.
+NVLink bytes per GPU per direction for RS+AG = 4 n (N-1) (bf16).
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2312_03549_b200 import _native as nat  # noqa: E402
+from paper_2312_03549_b200.comm import NcclComm  # noqa: E402
+from paper_2312_03549_b200.symm import SymmetricTensor  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--numel", type=int, default=104_857_600)
+    ap.add_argument("--iters", type=int, default=20)
+    a = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+    dev = torch.device("cuda", rank)
+    nat.load()
+    N = a.numel - a.numel % (16 * world)
+    n = N // world
+    pg = dist.group.WORLD
+    g = SymmetricTensor(N, torch.bfloat16, dev, pg)
+    p = SymmetricTensor(N, torch.bfloat16, dev, pg, zero=True)
+    fl = SymmetricTensor(64 * 8, torch.int32, dev, pg, zero=True)
+    g.tensor.normal_(0, 1e-3)
+    master = torch.randn(n, device=dev) * 0.02
+    m = torch.zeros(n, device=dev)
+    v = torch.zeros(n, device=dev)
+    red = torch.empty(n, dtype=torch.bfloat16, device=dev)
+    parts = torch.empty(nat.HOD_SUMSQ_PARTIALS, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    coef = torch.ones(1, device=dev)
+    torch.cuda.synchronize()
+    dist.barrier()
+    s = torch.cuda.current_stream()
+    epoch = [0]
+
+    def bucket(nvls):
+        bk = nat.P2PBucket()
+        if nvls:
+            bk.grad[0], bk.param[0] = g.multicast(), p.multicast()
+        else:
+            for q in range(world):
+                bk.grad[q], bk.param[q] = g.peer(q), p.peer(q)
+        for q in range(world):
+            bk.flags[q] = fl.peer(q)
+        bk.master, bk.exp_avg, bk.exp_avg_sq = master.data_ptr(), m.data_ptr(), v.data_ptr()
+        bk.err = err.data_ptr()
+        bk.shard_off, bk.n, bk.d, bk.rank, bk.nvls = rank * n, n, world, rank, int(nvls)
+        bk.slot, bk.timeout_ns = 0, 10_000_000_000
+        return bk
+
+    hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, 1)
+
+    def run_mode(mode, nvls):
+        bk = bucket(nvls)
+        epoch[0] += 1
+        bk.epoch = epoch[0]
+        if mode == nat.HOD_P2P_RS:
+            bk.reduced_out, bk.partials = red.data_ptr(), parts.data_ptr()
+        if mode == nat.HOD_P2P_ADAMW_AG:
+            bk.reduced_out, bk.clip_coef = red.data_ptr(), coef.data_ptr()
+        nat.call("hod_p2p_step", ctypes.byref(bk), mode, ctypes.byref(hp), s.cuda_stream)
+
+    comm = NcclComm(tuple(range(world)), rank, "bench")
+
+    def nccl_rs_ag():
+        base = g.tensor.data_ptr()
+        comm.reduce_scatter_bf16(base, base + 2 * rank * n, n, s)
+        comm.all_gather_bf16(p.tensor.data_ptr() + 2 * rank * n, p.tensor.data_ptr(), n, s)
+
+    def adamw_local():
+        nat.call("hod_adamw_bf16", master.data_ptr(), m.data_ptr(), v.data_ptr(), red.data_ptr(),
+                 p.tensor.data_ptr() + 2 * rank * n, n, ctypes.byref(hp), None, s.cuda_stream)
+
+    cases = {
+        "fused_p2p": lambda: run_mode(nat.HOD_P2P_FUSED, False),
+        "rs_p2p": lambda: run_mode(nat.HOD_P2P_RS, False),
+        "adamw_ag_p2p": lambda: run_mode(nat.HOD_P2P_ADAMW_AG, False),
+        "fused_nvls": lambda: run_mode(nat.HOD_P2P_FUSED, True),
+        "rs_nvls": lambda: run_mode(nat.HOD_P2P_RS, True),
+        "adamw_ag_nvls": lambda: run_mode(nat.HOD_P2P_ADAMW_AG, True),
+        "nccl_rs+ag": nccl_rs_ag,
+        "adamw_local": adamw_local,
+    }
+    out = {}
+    for name, fn in cases.items():
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) / a.iters], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        nvl = 4 * n * (world - 1) if "fused" in name or "nccl" in name else 2 * n * (world - 1)
+        if name == "adamw_local":
+            nvl = 0
+        out[name] = {"ms": round(ms, 4), "nvlink_GBps_per_dir": round(nvl / ms / 1e6, 1),
+                     "hbm_state_GBps": round(28 * n / ms / 1e6, 1)}
+    if int(err.item()):
+        out["error"] = int(err.item())
+    if rank == 0:
+        print(json.dumps({"world": world, "numel": N, "shard": n, "results": out}, indent=1))
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
