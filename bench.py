@@ -283,6 +283,7 @@ def run_ours(args) -> None:
     roof = {"kernel": "hod adamw_vec_kernel (K2)", "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
             "traffic": traffic, "traffic_source": prof, "peak_source": peak_src,
+            "traffic_launch_algorithmic_bytes": alg_per_launch,
             "algorithmic_bytes_per_launch": kbytes / max(1, n_launch),
             "avg_launch_ms": ktime / max(1, n_launch), "launches_timed": n_launch,
             "bytes_per_element": 28}
