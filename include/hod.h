@@ -89,6 +89,17 @@ long long hod_launch_count(void);
 int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket,
                   int64_t bucket_numel, float scale, int src_dtype, void* stream);
 
+/* ---- K1+K2 fused for d == 1 (no collective between pack and update) ------
+ * For every element of the bucket range [0, bucket_numel): g = bf16_rne(src*scale)
+ * (0 where no entry covers it), (* *clip_coef), AdamW on master/exp_avg/exp_avg_sq
+ * (bucket-indexed, bucket_numel elements each) and param = bf16_rne(master).
+ * Bit-identical to hod_pack_bf16 followed by hod_adamw_bf16 on the bucket;
+ * 28 B/element instead of 32. */
+int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel,
+                   float scale, int src_dtype, float* master, float* exp_avg,
+                   float* exp_avg_sq, uint16_t* param, const hod_adamw_params* hp,
+                   const float* clip_coef, void* stream);
+
 /* ---- K3: deterministic sum of squares of a bf16 shard -----
  * Writes HOD_SUMSQ_PARTIALS fp32 partial sums to partials[0..HOD_SUMSQ_PARTIALS)
  * (fixed grid, fixed order => bit-reproducible for a given n). */

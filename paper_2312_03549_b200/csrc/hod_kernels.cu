@@ -126,6 +126,70 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
+// K1+K2 fused (d == 1, no collective between them): the update reads the
+// gradient straight from the per-parameter tensors through the pack table,
+// with the same scale-then-RNE-to-bf16 the bucket would have held, so the
+// result is bit-identical to pack followed by AdamW while the 2+2 B/element
+// bucket round trip disappears (28 B/element instead of 32).
+// ---------------------------------------------------------------------------
+constexpr int kFusedTile = kThreads * 8;
+
+template <typename SrcT, bool kClip>
+__global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
+    const __grid_constant__ PackTable t, int64_t numel, float scale, float* __restrict__ p,
+    float* __restrict__ m, float* __restrict__ v, uint16_t* __restrict__ out, const AdamWConsts c,
+    const float* __restrict__ coef_ptr) {
+  const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
+  const int64_t n_tiles = (numel + kFusedTile - 1) / kFusedTile;
+  int e = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t a = tile * kFusedTile;
+    const int64_t b = min(a + kFusedTile, numel);
+    while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;  // CTA-uniform
+    const bool inside = e < t.n && t.off[e] <= a && b <= t.off[e] + t.numel[e];
+    if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kFusedTile) {
+      float g[8];
+      load8<SrcT>(t.src[e], a - t.off[e] + static_cast<int64_t>(threadIdx.x) * 8, g);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        g[k] = bf16_to_f32(f32_to_bf16(__fmul_rn(g[k], scale)));
+        if (kClip) g[k] = __fmul_rn(g[k], coef);
+      }
+      const int64_t iv = a / 8 + threadIdx.x;
+      float4* p4 = reinterpret_cast<float4*>(p) + 2 * iv;
+      float4* m4 = reinterpret_cast<float4*>(m) + 2 * iv;
+      float4* v4 = reinterpret_cast<float4*>(v) + 2 * iv;
+      float4 pa = p4[0], pb = p4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
+      float pf[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
+      float mf[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+      float vf[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+#pragma unroll
+      for (int k = 0; k < 8; ++k) adamw_elem(pf[k], mf[k], vf[k], g[k], c);
+      p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
+      p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
+      m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
+      m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
+      v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
+      v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
+      reinterpret_cast<uint4*>(out)[iv] = pack8(pf);
+    } else {
+      int ei = e;
+      for (int64_t i = a + threadIdx.x; i < b; i += kThreads) {
+        while (ei < t.n && t.off[ei] + t.numel[ei] <= i) ++ei;
+        float gi = 0.0f;
+        if (ei < t.n && t.off[ei] <= i)
+          gi = bf16_to_f32(f32_to_bf16(__fmul_rn(load_src<SrcT>(t.src[ei], i - t.off[ei]), scale)));
+        if (kClip) gi = __fmul_rn(gi, coef);
+        float pi = p[i], mi = m[i], vi = v[i];
+        adamw_elem(pi, mi, vi, gi, c);
+        p[i] = pi; m[i] = mi; v[i] = vi;
+        out[i] = f32_to_bf16(pi);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K2: AdamW.  Eight elements per thread per iteration: one 16-byte load of
 // bf16 grad, two 16-byte loads each of master/m/v; stores mirror them plus a
 // 16-byte bf16 param store.  28 B/element algorithmic traffic.
@@ -279,6 +343,55 @@ __global__ void clip_coef_kernel(const float* sumsq, float max_norm, float* coef
   if (norm) *norm = nrm;
 }
 
+// Validate a pack table once on the host and split it into windows of at
+// most HOD_PACK_MAX_ENTRIES entries; each window covers the destination range
+// [lo, hi) from its first entry to the next window's first entry (the first
+// window starts at 0, the last ends at bucket_numel, so gaps/padding are
+// always covered).  `fn(table, lo, span)` launches one kernel per window.
+template <typename Fn>
+static int for_each_window(const char* who, const hod_pack_entry* entries, int n_entries,
+                           int64_t bucket_numel, int src_dtype, Fn&& fn) {
+  if (bucket_numel < 0 || n_entries < 0 || (n_entries > 0 && !entries)) {
+    set_error("%s: bad arguments", who); return HOD_EINVAL;
+  }
+  if (src_dtype != HOD_DTYPE_BF16 && src_dtype != HOD_DTYPE_F32) {
+    set_error("%s: unknown src_dtype %d", who, src_dtype); return HOD_EINVAL;
+  }
+  if (bucket_numel == 0) return HOD_OK;
+  int64_t prev_end = 0;
+  for (int i = 0; i < n_entries; ++i) {
+    const hod_pack_entry& e = entries[i];
+    if (!e.src || e.numel < 0 || e.dst_offset < prev_end || e.dst_offset + e.numel > bucket_numel) {
+      set_error("%s: entry %d out of order or out of bounds", who, i); return HOD_EINVAL;
+    }
+    prev_end = e.dst_offset + e.numel;
+  }
+  int first = 0;
+  do {
+    const int cnt = (n_entries - first) < HOD_PACK_MAX_ENTRIES ? (n_entries - first) : HOD_PACK_MAX_ENTRIES;
+    const int64_t lo = (first == 0) ? 0 : entries[first].dst_offset;
+    const int64_t hi = (first + cnt < n_entries) ? entries[first + cnt].dst_offset : bucket_numel;
+    PackTable t;
+    memset(&t, 0, sizeof(t));
+    t.n = cnt;
+    for (int i = 0; i < cnt; ++i) {
+      const hod_pack_entry& e = entries[first + i];
+      t.off[i] = e.dst_offset - lo;
+      t.numel[i] = e.numel;
+      t.src[i] = e.src;
+      // the vector paths read 8 elements at (tile_start - off): needs off % 8 == 0
+      if (aligned16(e.src) && ((e.dst_offset - lo) % 8 == 0)) t.vec_ok |= (1ull << i);
+    }
+    if (hi - lo > 0) {
+      if (lo % 8) { set_error("%s: window start %lld not a multiple of 8", who, (long long)lo); return HOD_EALIGN; }
+      const int rc = fn(t, lo, hi - lo);
+      if (rc) return rc;
+    }
+    first += cnt;
+  } while (first < n_entries);
+  return HOD_OK;
+}
+
 }  // namespace hod
 
 using namespace hod;
@@ -293,62 +406,51 @@ long long hod_launch_count(void) { return g_launches.load(std::memory_order_rela
 
 int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket,
                   int64_t bucket_numel, float scale, int src_dtype, void* stream) {
-  if (!bucket || bucket_numel < 0 || n_entries < 0 || (n_entries > 0 && !entries)) {
-    set_error("hod_pack_bf16: bad arguments"); return HOD_EINVAL;
-  }
-  if (src_dtype != HOD_DTYPE_BF16 && src_dtype != HOD_DTYPE_F32) {
-    set_error("hod_pack_bf16: unknown src_dtype %d", src_dtype); return HOD_EINVAL;
-  }
+  if (!bucket) { set_error("hod_pack_bf16: bad arguments"); return HOD_EINVAL; }
   if (!aligned16(bucket)) { set_error("hod_pack_bf16: bucket not 16-byte aligned"); return HOD_EALIGN; }
-  if (bucket_numel == 0) return HOD_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // validate ordering / bounds once on the host
-  int64_t prev_end = 0;
-  for (int i = 0; i < n_entries; ++i) {
-    const hod_pack_entry& e = entries[i];
-    if (!e.src || e.numel < 0 || e.dst_offset < prev_end || e.dst_offset + e.numel > bucket_numel) {
-      set_error("hod_pack_bf16: entry %d out of order or out of bounds", i); return HOD_EINVAL;
+  return for_each_window("hod_pack_bf16", entries, n_entries, bucket_numel, src_dtype,
+                         [&](const PackTable& t, int64_t lo, int64_t span) {
+    if (!aligned16(bucket + lo)) {
+      set_error("hod_pack_bf16: window start %lld not 16-byte aligned", (long long)lo); return HOD_EALIGN;
     }
-    prev_end = e.dst_offset + e.numel;
+    const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, 4);
+    count_launch(1);
+    if (src_dtype == HOD_DTYPE_BF16)
+      pack_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
+    else
+      pack_kernel<float><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
+    return cuda_status(cudaGetLastError(), "hod_pack_bf16 launch");
+  });
+}
+
+int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel, float scale,
+                   int src_dtype, float* master, float* exp_avg, float* exp_avg_sq, uint16_t* param,
+                   const hod_adamw_params* hp, const float* clip_coef, void* stream) {
+  if (!master || !exp_avg || !exp_avg_sq || !param || !hp) {
+    set_error("hod_pack_adamw: bad arguments"); return HOD_EINVAL;
   }
-  // Split long tables into windows of HOD_PACK_MAX_ENTRIES; each launch covers
-  // the destination range [lo, hi) between its first and the next window.
-  int first = 0;
-  do {
-    const int cnt = (n_entries - first) < HOD_PACK_MAX_ENTRIES ? (n_entries - first) : HOD_PACK_MAX_ENTRIES;
-    const int64_t lo = (first == 0) ? 0 : entries[first].dst_offset;
-    const int64_t hi = (first + cnt < n_entries) ? entries[first + cnt].dst_offset : bucket_numel;
-    PackTable t;
-    memset(&t, 0, sizeof(t));
-    t.n = cnt;
-    const size_t esz = src_dtype == HOD_DTYPE_BF16 ? 2 : 4;
-    for (int i = 0; i < cnt; ++i) {
-      const hod_pack_entry& e = entries[first + i];
-      t.off[i] = e.dst_offset - lo;
-      t.numel[i] = e.numel;
-      // the vector path reads 8 elements at (tile_start - off) which is a
-      // multiple of 8 only when off is; require both for the fast path
-      const bool ok = aligned16(e.src) && ((e.dst_offset - lo) % 8 == 0) && (esz * 8) % 16 == 0;
-      t.src[i] = e.src;
-      if (ok) t.vec_ok |= (1ull << i);
+  if (hp->step < 1) { set_error("hod_pack_adamw: step must be >= 1"); return HOD_EINVAL; }
+  if (!aligned16(master) || !aligned16(exp_avg) || !aligned16(exp_avg_sq) || !aligned16(param)) {
+    set_error("hod_pack_adamw: state/param buffers must be 16-byte aligned"); return HOD_EALIGN;
+  }
+  const AdamWConsts c = fold_adamw(*hp);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return for_each_window("hod_pack_adamw", entries, n_entries, bucket_numel, src_dtype,
+                         [&](const PackTable& t, int64_t lo, int64_t span) {
+    const int grid = grid_for((span + kFusedTile - 1) / kFusedTile, 1, 8);
+    count_launch(1);
+#define HOD_PA_LAUNCH(T, CLIP) \
+    pack_adamw_kernel<T, CLIP><<<grid, kThreads, 0, s>>>(t, span, scale, master + lo, exp_avg + lo, \
+                                                        exp_avg_sq + lo, param + lo, c, clip_coef)
+    if (src_dtype == HOD_DTYPE_BF16) {
+      if (clip_coef) HOD_PA_LAUNCH(uint16_t, true); else HOD_PA_LAUNCH(uint16_t, false);
+    } else {
+      if (clip_coef) HOD_PA_LAUNCH(float, true); else HOD_PA_LAUNCH(float, false);
     }
-    const int64_t span = hi - lo;
-    if (span > 0) {
-      if (!aligned16(bucket + lo)) {
-        set_error("hod_pack_bf16: window start %lld not 16-byte aligned", (long long)lo); return HOD_EALIGN;
-      }
-      const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, 4);
-      count_launch(1);
-      if (src_dtype == HOD_DTYPE_BF16)
-        pack_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
-      else
-        pack_kernel<float><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
-      const int rc = cuda_status(cudaGetLastError(), "hod_pack_bf16 launch");
-      if (rc) return rc;
-    }
-    first += cnt;
-  } while (first < n_entries);
-  return HOD_OK;
+#undef HOD_PA_LAUNCH
+    return cuda_status(cudaGetLastError(), "hod_pack_adamw launch");
+  });
 }
 
 int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) {

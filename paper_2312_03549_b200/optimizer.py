@@ -382,10 +382,23 @@ class DistributedOptimizer:
             entries[k].numel = s.numel
             entries[k].dst_offset = s.offset
         bucket_ptr = _ptr(self.grad_buffer) + 2 * b.start
+        src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
+        if self.backend == "none" and self.clip is None and not self.keep_reduced:
+            # d == 1: nothing to exchange, so K1 and K2 fuse (no bucket round trip)
+            off = self._shard_off[bi]
+            hp = self._hp()
+            t0 = self._timed_event(self.s_pack)
+            nat.call("hod_pack_adamw", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale),
+                     dtype, _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
+                     _ptr(self.exp_avg_sq) + 4 * off, _ptr(self.param_buffer) + 2 * b.start,
+                     ctypes.byref(hp), None, nat.stream_ptr(self.s_pack))
+            self._timed_close("pack_adamw", t0, self.s_pack, (src_bytes + 26) * b.numel)
+            self._ev_params[bi].record(self.s_pack)
+            self._launched[bi] = True
+            return
         t0 = self._timed_event(self.s_pack)
         nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
                  ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
-        src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
         self._timed_close("pack", t0, self.s_pack, (src_bytes + 2) * b.numel)
         self._ev_packed[bi].record(self.s_pack)
         self._launched[bi] = True

@@ -67,6 +67,40 @@ def test_pack_many_entries_splits_windows(oracle, native):
     np.testing.assert_array_equal(got, want)
 
 
+@pytest.mark.parametrize("src_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("clip", [None, 0.3])
+def test_pack_adamw_fused_equals_pack_then_adamw(oracle, native, src_dtype, clip):
+    """K1+K2 fused (d == 1) is bit-identical to pack -> AdamW on the bucket."""
+    gs = odd_tensors()
+    layout = build_bucket_layout(gs.numels, 150_000, dp=1)
+    gen = torch.Generator(device=DEV).manual_seed(21)
+    grads = [torch.randn(t.shape, generator=gen, device=DEV).mul_(1e-2).to(src_dtype) for t in gs.tensors]
+    coef = None if clip is None else torch.tensor([clip], device=DEV)
+    for b in layout.buckets:
+        gl = [grads[s.index].reshape(-1) for s in b.slots]
+        offs = [s.offset for s in b.slots]
+        master = torch.randn(b.numel, generator=gen, device=DEV).mul_(0.02)
+        m = torch.rand(b.numel, generator=gen, device=DEV).mul_(1e-3)
+        v = torch.rand(b.numel, generator=gen, device=DEV).mul_(1e-6)
+        cm, cv, cp = master.cpu().numpy().copy(), m.cpu().numpy().copy(), v.cpu().numpy().copy()
+        out = torch.empty(b.numel, dtype=torch.bfloat16, device=DEV)
+        entries = (nat.PackEntry * len(gl))()
+        for k, (g, off) in enumerate(zip(gl, offs)):
+            entries[k].src, entries[k].numel, entries[k].dst_offset = g.data_ptr(), g.numel(), off
+        hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, 7)
+        dt = nat.HOD_DTYPE_F32 if src_dtype == torch.float32 else nat.HOD_DTYPE_BF16
+        nat.call("hod_pack_adamw", entries, len(gl), b.numel, ctypes.c_float(0.5), dt, master.data_ptr(),
+                 m.data_ptr(), v.data_ptr(), out.data_ptr(), ctypes.byref(hp),
+                 None if coef is None else coef.data_ptr(), 0)
+        torch.cuda.synchronize()
+        cpu = [g.cpu().numpy() if src_dtype == torch.float32 else u16(g) for g in gl]
+        packed = oracle.pack(cpu, offs, b.numel, 0.5)
+        want = oracle.adamw(cm, cv, cp, packed, 7, coef=None if clip is None else np.float32(clip))
+        np.testing.assert_array_equal(u16(out), want)
+        np.testing.assert_array_equal(master.cpu().numpy().view(np.uint32), cm.view(np.uint32))
+        np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), cp.view(np.uint32))
+
+
 def _adamw_gpu(master, m, v, grad, n, step, coef=None, out_offset=0):
     out = torch.empty(n + out_offset, dtype=torch.bfloat16, device=DEV)
     hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, step)

@@ -31,15 +31,17 @@ def _oracle_state(oracle, layout, params_cpu):
     return state
 
 
+@pytest.mark.parametrize("keep_reduced", [False, True])   # False: K1+K2 fused at d = 1
 @pytest.mark.parametrize("config,grad_dtype,clip,bucket",
                          [("toy", torch.float32, None, 25_000_000),
                           ("toy", torch.bfloat16, 1.0, 2_000_000),
                           ("odd", torch.bfloat16, 0.01, 100_000),
-                          ("odd", torch.float32, None, 10**9)])
-def test_single_rank_steps_match_oracle(oracle, native, config, grad_dtype, clip, bucket):
+                          ("odd", torch.float32, None, 10**9),
+                          ("odd", torch.bfloat16, None, 70_000)])
+def test_single_rank_steps_match_oracle(oracle, native, config, grad_dtype, clip, bucket, keep_reduced):
     gs = config_gradset(config)
     p0 = init_params(gs, DEV)
-    opt = DistributedOptimizer(p0, bucket_size=bucket, clip=clip)
+    opt = DistributedOptimizer(p0, bucket_size=bucket, clip=clip, keep_reduced=keep_reduced)
     L = opt.layout
     state = _oracle_state(oracle, L, [p.cpu().numpy() for p in p0])
     for step in (1, 2, 3):
@@ -78,7 +80,7 @@ def test_single_rank_steps_match_oracle(oracle, native, config, grad_dtype, clip
 
 def test_padding_stays_zero_and_params_alias(native):
     gs = config_gradset("odd")
-    opt = DistributedOptimizer(init_params(gs, DEV), bucket_size=50_000)
+    opt = DistributedOptimizer(init_params(gs, DEV), bucket_size=50_000, keep_reduced=True)
     opt.step(make_grads(gs, 1, 0, DEV))
     torch.cuda.synchronize()
     pad_mask = torch.ones(opt.layout.total_numel, dtype=torch.bool, device=DEV)
