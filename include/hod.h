@@ -80,6 +80,12 @@ int hod_abi_version(void);
 const char* hod_last_error(void);
 /* number of kernels this library has launched in the process (all streams) */
 long long hod_launch_count(void);
+/* Cap every subsequent launch of the calling thread at `max_ctas` CTAs
+ * (0 = no cap).  The overlapped optimizer sets it while backward GEMMs run so
+ * its kernels occupy a bounded slice of the 148 SMs (pair with cuBLAS's SM
+ * carve-out); partial-sum kernels use min(cap, HOD_SUMSQ_PARTIALS) CTAs and
+ * zero the unused partial slots. */
+int hod_set_grid_limit(int max_ctas);
 
 /* ---- K1: bucket pack + dp-scale + bf16 cast ---------------
  * bucket[dst_offset + i] = bf16_rne(float(src[i]) * scale), zeros elsewhere.

@@ -22,7 +22,7 @@ HOD_DTYPE_F32 = 1
 
 # every symbol include/hod.h declares (checked by tests/test_abi.py)
 EXPORTED = (
-    "hod_abi_version", "hod_last_error", "hod_launch_count",
+    "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
     "hod_pack_bf16", "hod_pack_adamw", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
     "hod_adamw_bf16", "hod_adamw_f32",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
@@ -83,6 +83,7 @@ def load(build_if_missing: bool = True):
         "hod_abi_version": ([], I),
         "hod_last_error": ([], ctypes.c_char_p),
         "hod_launch_count": ([], ctypes.c_longlong),
+        "hod_set_grid_limit": ([I], I),
         "hod_pack_bf16": ([ctypes.POINTER(PackEntry), I, P, I64, F, I, P], I),
         "hod_sumsq_bf16": ([P, I64, P, P], I),
         "hod_pack_adamw": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, P, P, P,

@@ -76,11 +76,23 @@ __device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g
   p = __fsub_rn(p, __fmul_rn(c.step_size, __fdiv_rn(m, den)));
 }
 
+// CTA cap set by hod_set_grid_limit (0 = none): lets the optimizer's kernels
+// co-run with the backward GEMMs on a bounded slice of the SMs.
+int grid_limit();
+
 inline int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 8) {
   int64_t need = (work_items + per_block - 1) / per_block;
   int64_t cap = static_cast<int64_t>(kSMs) * max_blocks_per_sm;
+  if (grid_limit() > 0 && grid_limit() < cap) cap = grid_limit();
   if (need < 1) need = 1;
   return static_cast<int>(need < cap ? need : cap);
+}
+
+// Grid of the kernels that emit HOD_SUMSQ_PARTIALS per-CTA partials: fixed
+// (reproducible) for a given limit; CTA 0 zero-fills the unused slots.
+inline int partials_grid() {
+  const int lim = grid_limit();
+  return (lim > 0 && lim < HOD_SUMSQ_PARTIALS) ? lim : HOD_SUMSQ_PARTIALS;
 }
 
 inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }

@@ -20,6 +20,9 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+static thread_local int g_grid_limit = 0;
+int grid_limit() { return g_grid_limit; }
+
 void set_error(const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -325,6 +328,8 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const uint16_t* __restr
   }
   const float s = block_sum(acc);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  if (blockIdx.x == 0)
+    for (int i = gridDim.x + threadIdx.x; i < HOD_SUMSQ_PARTIALS; i += blockDim.x) partials[i] = 0.0f;
 }
 
 __global__ void sum_partials_kernel(const float* __restrict__ partials, int64_t n, float* out) {
@@ -404,6 +409,12 @@ const char* hod_last_error(void) { return g_err; }
 
 long long hod_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
+int hod_set_grid_limit(int max_ctas) {
+  if (max_ctas < 0) { set_error("hod_set_grid_limit: negative limit"); return HOD_EINVAL; }
+  g_grid_limit = max_ctas;
+  return HOD_OK;
+}
+
 int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket,
                   int64_t bucket_numel, float scale, int src_dtype, void* stream) {
   if (!bucket) { set_error("hod_pack_bf16: bad arguments"); return HOD_EINVAL; }
@@ -456,7 +467,7 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
 int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) {
   if (!partials || n < 0 || (n > 0 && !x)) { set_error("hod_sumsq_bf16: bad arguments"); return HOD_EINVAL; }
   count_launch(1);
-  sumsq_kernel<<<HOD_SUMSQ_PARTIALS, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
+  sumsq_kernel<<<partials_grid(), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
   return cuda_status(cudaGetLastError(), "hod_sumsq_bf16 launch");
 }
 

@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const FusedArgs a, c
   if (kMode == 1 && a.partials) {
     const float s = block_sum_f(ss);
     if (threadIdx.x == 0) a.partials[blockIdx.x] = s;
+    if (blockIdx.x == 0)
+      for (int i = gridDim.x + threadIdx.x; i < HOD_SUMSQ_PARTIALS; i += blockDim.x) a.partials[i] = 0.0f;
   }
   if (kMode != 1) __threadfence_system();  // remote param stores performed before any later signal
 }
@@ -390,7 +392,7 @@ int hod_p2p_step(const hod_p2p_bucket* bk, int mode, const hod_adamw_params* hp,
   if (mode == HOD_P2P_RS && !a.reduced_out && !a.partials) { set_error("hod_p2p_step: RS writes nothing"); return HOD_EINVAL; }
   const AdamWConsts c = (mode != HOD_P2P_RS) ? fold_adamw(*hp) : AdamWConsts{};
   // RS keeps a FIXED grid so its sum-of-squares partials are reproducible
-  const int grid = (mode == HOD_P2P_RS) ? HOD_SUMSQ_PARTIALS : grid_for(a.n / 8, kThreads, 4);
+  const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(a.n / 8, kThreads, 4);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool nv = bk->nvls != 0;
   if (mode == HOD_P2P_FUSED) {

@@ -120,7 +120,8 @@ class DistributedOptimizer:
                  bucket_size: int = 25_000_000, dp_group: DPGroup | None = None,
                  norm_ranks=None, grad_scale: float | None = None, backend: str = "auto",
                  device=None, param_align: int = 64, process_group=None, norm_group=None,
-                 keep_reduced: bool = False, barrier_timeout_s: float = 20.0):
+                 keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
+                 sm_budget: int | None = None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -145,6 +146,9 @@ class DistributedOptimizer:
             raise InfeasibleConfigError(f"{backend} supports at most {nat.HOD_P2P_MAX_RANKS} ranks")
         self.backend = backend
         self.keep_reduced = keep_reduced
+        # CTAs per launch while backward still runs (None = whole GPU); the last
+        # bucket and the post-backward phase always get the whole GPU
+        self.sm_budget = sm_budget
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
 
@@ -196,9 +200,12 @@ class DistributedOptimizer:
         fill_master_shards(L, init_params, self.shard_index, self.master)
 
         # streams / events (one set per bucket, reused every step)
-        self.s_pack = torch.cuda.Stream(device=dev)
-        self.s_comm = torch.cuda.Stream(device=dev) if self.dp > 1 else self.s_pack
-        self.s_opt = torch.cuda.Stream(device=dev) if self.dp > 1 else self.s_pack
+        # high-priority streams: when an SM frees up between backward GEMM
+        # tiles, the optimizer's CTAs are dispatched first
+        hi = torch.cuda.Stream.priority_range()[1] if hasattr(torch.cuda.Stream, "priority_range") else -1
+        self.s_pack = torch.cuda.Stream(device=dev, priority=hi)
+        self.s_comm = torch.cuda.Stream(device=dev, priority=hi) if self.dp > 1 else self.s_pack
+        self.s_opt = torch.cuda.Stream(device=dev, priority=hi) if self.dp > 1 else self.s_pack
         nb = len(L.buckets)
         self._ev_packed = [torch.cuda.Event() for _ in range(nb)]
         self._ev_reduced = [torch.cuda.Event() for _ in range(nb)]
@@ -355,6 +362,14 @@ class DistributedOptimizer:
         return _ptr(self.grad_buffer) + 2 * lo, hi - lo
 
     def _launch_bucket(self, bi: int) -> None:
+        last = sum(self._launched) == len(self._launched) - 1
+        nat.call("hod_set_grid_limit", 0 if (last or not self.sm_budget) else int(self.sm_budget))
+        try:
+            self._launch_bucket_body(bi)
+        finally:
+            nat.call("hod_set_grid_limit", 0)
+
+    def _launch_bucket_body(self, bi: int) -> None:
         b = self.layout.buckets[bi]
         grads = self._pending_grads[bi]
         cur = torch.cuda.current_stream(self.device)

@@ -1,0 +1,181 @@
+"""Exposed-collective measurement of the overlapped optimizer.
+
+    torchrun --nproc-per-node N tools/overlap_bench.py [--config gpt1.3b] [--tokens 8192]
+
+A synthetic backward produces real gradients with cuBLAS GEMMs on the compute
+stream, layer by layer in reverse registration order: for every weight W
+(out x in) with activations X (tokens x in) and output grads dY (tokens x out)
+it runs dX = dY @ W and dW = dY^T @ X (bf16), and hands dW to
+``DistributedOptimizer.grad_ready`` the moment it is enqueued — buckets fill
+in backward order and their pack -> RS -> AdamW -> AG run on side streams while
+the remaining layers' GEMMs execute.  Three timings (CUDA events, max over
+ranks):
+
+  T_bwd      backward GEMMs alone
+  T_opt      optimizer step alone (grads already resident)
+  T_overlap  backward with the optimizer overlapped, up to params ready
+exposed = T_overlap - T_bwd  (collective + update time not hidden by compute),
+reported as a fraction of T_overlap (north-star target <= 10 %).
+The same exposed time is fed to the reference simulator's post-flush charge
+(``simulate_iteration(exposed_dp_sync=...)``, §8f.1) for the config's scenario.
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2312_03549_b200 import DistributedOptimizer  # noqa: E402
+from paper_2312_03549_b200.comm import DPGroup  # noqa: E402
+from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
+from paper_2312_03549_b200.synthetic import init_params  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="gpt1.3b")
+    ap.add_argument("--tokens", type=int, default=8192, help="micro-batch tokens per GPU (b*s)")
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--backend", default="auto")
+    ap.add_argument("--clip", type=float, default=0.0)
+    ap.add_argument("--bucket-size", type=int, default=25_000_000)
+    ap.add_argument("--sm-budget", type=int, default=0,
+                    help="CTAs per optimizer launch during backward; the backward GEMMs get the "
+                         "same number of SMs carved out (torch._C._set_sm_carveout_experimental)")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    gs = config_gradset(a.config)
+    p0 = init_params(gs, dev)
+    opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None,
+                               dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
+                               sm_budget=a.sm_budget or None)
+    del p0
+    T = a.tokens
+    # 2-D weights get GEMMs; 1-D (norm) weights get a tiny elementwise grad
+    acts = {}
+    for t in gs.tensors:
+        if len(t.shape) == 2:
+            out_f, in_f = t.shape
+            for dim in (out_f, in_f):
+                if dim not in acts:
+                    acts[dim] = torch.randn(T, dim, device=dev, dtype=torch.bfloat16)
+    grads = [torch.empty(t.shape, device=dev, dtype=torch.bfloat16) for t in gs.tensors]
+    order = [s.index for b in opt.layout.buckets for s in b.slots]   # backward order
+
+    def backward(feed_opt: bool):
+        for i in order:
+            t = gs.tensors[i]
+            if len(t.shape) == 2:
+                out_f, in_f = t.shape
+                dy, x = acts[out_f], acts[in_f]
+                if t.name.endswith("embed.weight") or "embed_tokens" in t.name:
+                    grads[i].normal_(0, 1e-3)          # embedding grad is a scatter, not a GEMM
+                else:
+                    torch.matmul(dy, opt.params[i], out=None)            # dX = dY @ W
+                    torch.matmul(dy.t(), x, out=grads[i])                # dW = dY^T @ X
+            else:
+                grads[i].normal_(0, 1e-3)
+            if feed_opt:
+                opt.grad_ready(i, grads[i])
+
+    def timed(fn):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.iters):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.iters
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms
+
+    if a.sm_budget:
+        # the SM carve-out is honoured by the cuBLASLt path
+        torch.backends.cuda.preferred_blas_library("cublaslt")
+
+    def carve(on: bool):
+        if a.sm_budget and hasattr(torch._C, "_set_sm_carveout_experimental"):
+            torch._C._set_sm_carveout_experimental(a.sm_budget if on else None)
+
+    def backward_carved():
+        carve(True)
+        backward(False)
+        carve(False)
+
+    def overlapped():
+        carve(True)
+        opt.begin_step()
+        backward(True)
+        opt.finish_step()        # current stream waits for every bucket's params
+        carve(False)
+
+    for _ in range(2):           # warm-up all three modes
+        backward(False)
+        opt.step(grads)
+        overlapped()
+    t_bwd = timed(lambda: backward(False))
+    t_bwd_carved = timed(backward_carved) if a.sm_budget else t_bwd
+    t_opt = timed(lambda: opt.step(grads))
+    t_ovl = timed(overlapped)
+    # one instrumented overlapped step: where did the optimizer kernels run?
+    base = torch.cuda.Event(enable_timing=True)
+    end_bwd = torch.cuda.Event(enable_timing=True)
+    opt.enable_kernel_timing(True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    base.record()
+    carve(True)
+    opt.begin_step()
+    backward(True)
+    end_bwd.record()
+    opt.finish_step()
+    carve(False)
+    torch.cuda.synchronize()
+    bwd_end_ms = base.elapsed_time(end_bwd)
+    spans = [(name, base.elapsed_time(e0), base.elapsed_time(e1)) for name, e0, e1, _ in opt._ktiming]
+    opt.enable_kernel_timing(False)
+    busy_in_bwd = sum(max(0.0, min(e, bwd_end_ms) - s0) for _, s0, e in spans if s0 < bwd_end_ms)
+    busy_total = sum(e - s0 for _, s0, e in spans)
+    first_start = min((s0 for _, s0, _ in spans), default=0.0)
+    opt.check_health()
+    exposed = max(0.0, t_ovl - t_bwd)
+    flops = sum(4 * T * t.shape[0] * t.shape[1] for t in gs.tensors if len(t.shape) == 2
+                and "embed" not in t.name)
+    doc = {"config": a.config, "world": world, "backend": opt.backend, "tokens_per_gpu": T,
+           "sm_budget": a.sm_budget,
+           "clip": a.clip or None, "buckets": len(opt.layout.buckets), "bucket_size": a.bucket_size,
+           "t_backward_ms": round(t_bwd, 3), "t_backward_carved_ms": round(t_bwd_carved, 3),
+           "t_optimizer_alone_ms": round(t_opt, 3),
+           "timeline": {"backward_end_ms": round(bwd_end_ms, 3), "first_opt_kernel_start_ms": round(first_start, 3),
+                        "last_opt_kernel_end_ms": round(max((e for _, _, e in spans), default=0.0), 3),
+                        "opt_kernel_ms_inside_backward": round(busy_in_bwd, 3),
+                        "opt_kernel_ms_total": round(busy_total, 3)},
+           "t_overlapped_ms": round(t_ovl, 3), "exposed_ms": round(exposed, 3),
+           "exposed_frac_of_step": round(exposed / t_ovl, 4),
+           "hidden_frac_of_optimizer": round(1 - exposed / t_opt, 4) if t_opt > 0 else None,
+           "backward_tflops": round(flops / (t_bwd / 1e3) / 1e12, 1)}
+    if rank == 0:
+        print(json.dumps(doc))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
