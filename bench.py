@@ -246,14 +246,38 @@ def run_ours(args) -> None:
     world, rank, local = _dist_setup(args)
     cfg = CONFIGS[args.config]
     clip = cfg["clip"] if args.clip is None else (None if args.clip <= 0 else args.clip)
-    gs = config_gradset(args.config)
     dev = torch.device("cuda", local)
     gdtype = torch.float32 if cfg["grad_dtype"] == "f32" else torch.bfloat16
+    scen = None
+    if args.scenario:
+        # BASELINE config 4: PP x DP from the reference-compatible planner; every
+        # stage updates its own gradient set, the clip norm spans the world
+        import paper_2312_03549_b200 as hp
+        from paper_2312_03549_b200.scenario_run import make_optimizer, setup_rank
 
-    p0 = init_params(gs, dev)
-    group = DPGroup(tuple(range(world)), rank)
-    opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group,
-                               backend=args.backend)
+        scenario = hp.load_scenario(args.scenario)
+        sr = setup_rank(scenario, rank)
+        gs = sr.gradset
+        clip = 1.0 if args.clip is None else (None if args.clip <= 0 else args.clip)
+        p0 = init_params(gs, dev)
+        opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=clip, backend=args.backend)
+        stage_params = {sr.placement.stage: gs.total}
+        gathered = [None] * world
+        import torch.distributed as dist
+
+        dist.all_gather_object(gathered, stage_params)
+        totals = {}
+        for dct in gathered:
+            totals.update(dct)
+        scen = {"scenario": Path(args.scenario).name, "stage_layers": None, "stage_params": totals,
+                "placement": sr.placement.to_json_dict()}
+        scen["stage_layers"] = list(hp.partition_scenario(scenario).stage_layers)
+    else:
+        gs = config_gradset(args.config)
+        p0 = init_params(gs, dev)
+        group = DPGroup(tuple(range(world)), rank)
+        opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group,
+                                   backend=args.backend)
     del p0
     torch.cuda.empty_cache()
     grads = make_grads(gs, 1, rank, dev, dtype=gdtype)
@@ -280,7 +304,9 @@ def run_ours(args) -> None:
     ms = _max_over_ranks(ms, world)
     kt = opt.kernel_timing()
     opt.enable_kernel_timing(False)
-    params_per_step = gs.total  # every parameter of the set updated once per step
+    # every parameter of the set (of every stage, for a PP x DP scenario) is
+    # updated once per step
+    params_per_step = sum(scen["stage_params"].values()) if scen else gs.total
     value = params_per_step / (ms / 1e3)
 
     # ---- roofline of the dominant kernel ----------------------------------
@@ -298,11 +324,11 @@ def run_ours(args) -> None:
             "algorithmic_bytes_per_launch": kbytes / max(1, n_launch),
             "avg_launch_ms": ktime / max(1, n_launch), "launches_timed": n_launch,
             "bytes_per_element": 28}
-    if dom in ("fused", "adamw_ag", "rs") and world > 1:
+    if dom in ("fused", "adamw_ag", "rs") and opt.dp > 1:
         # the collective half dominates: report NVLink per direction per GPU
         # (RS in + AG out for p2p = 2(d-1) B each per owned element)
-        elems = kbytes / 28 if dom != "rs" else kbytes / (2 * world + 2)
-        per_elem = {"fused": 4, "adamw_ag": 2, "rs": 2}[dom] * (world - 1)
+        elems = kbytes / 28 if dom != "rs" else kbytes / (2 * opt.dp + 2)
+        per_elem = {"fused": 4, "adamw_ag": 2, "rs": 2}[dom] * (opt.dp - 1)
         nvl = elems * per_elem / (ktime / 1e3) / 1e9 if ktime > 0 else None
         roof.update({"bound": "nvlink", "achieved": nvl, "peak": 900.0,
                      "frac": nvl / 900.0 if nvl else None, "peak_source": "NVLink 5 nominal 900 GB/s/dir "
@@ -312,15 +338,15 @@ def run_ours(args) -> None:
     kernels = {k: {"launches": n, "ms_total": t, "GBps": (b / (t / 1e3)) / 1e9 if t else None}
                for k, (n, t, b) in kt.items()}
     # step-level roofline: max(HBM bytes / peak, NVLink bytes / 900 GB/s)
-    d = world
-    P = params_per_step
+    d = opt.dp
+    P = gs.total  # this rank's stage
     src_b = 4 if gdtype == torch.float32 else 2
     if d == 1 and not clip:   # K1+K2 fuse: grad read + 24 B state + 2 B param, no bucket
         hbm_bytes = (src_b + 26) * P
     else:
         hbm_bytes = (src_b + 2) * P + 28 * P / d + (2 * P / d if clip else 0)
     nvl_bytes = 4 * P * (d - 1) / d
-    t_roof = max(hbm_bytes / (peak * 1e9), nvl_bytes / 900e9)
+    t_roof = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / 900e9), world)
     step_roof = {"t_roof_ms": t_roof * 1e3, "frac": (t_roof * 1e3) / ms,
                  "hbm_bytes_per_gpu": hbm_bytes, "nvlink_bytes_per_gpu_per_dir": nvl_bytes,
                  "bound": "hbm" if hbm_bytes / (peak * 1e9) >= nvl_bytes / 900e9 else "nvlink"}
@@ -360,9 +386,13 @@ def run_ours(args) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16-grads/f32-adamw", "data": "synthetic",
-            "config": {"workload": cfg["desc"], "config": args.config, "params": P,
+            "config": {"workload": (f"scenario {scen['scenario']}: GPT stages {scen['stage_layers']} "
+                                    "(reference self-adapting partition), PP x DP, world clip norm"
+                                    if scen else cfg["desc"]),
+                       "config": "scenario" if scen else args.config, "params": params_per_step,
+                       "scenario": scen,
                        "buckets": len(opt.layout.buckets), "bucket_size": args.bucket_size,
-                       "dp": world, "clip": clip, "backend": opt.backend,
+                       "dp": opt.dp, "clip": clip, "backend": opt.backend,
                        "l2": "inputs (~%.0f GB) >> 126 MB L2, no flush needed" % (hbm_bytes / 1e9)},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
@@ -382,6 +412,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="gpt1.3b", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scenario", default=None,
+                    help="scenario JSON (reference schema) for a PP x DP run, e.g. "
+                         "scenarios/gpt13b_pp2_dp4_hybrid.json (BASELINE config 4, 8 GPUs)")
     ap.add_argument("--bucket-size", type=int, default=25_000_000)
     ap.add_argument("--backend", default="auto")
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")

@@ -128,3 +128,71 @@ def test_multi_rank_parity(oracle, tmp_path, n, config, gd, bucket, clip, backen
     # the NVSwitch reduction order are checked against the fp64 sum bound
     check(oracle, tmp_path, n, config, gd, 2, clip > 0,
           exact_rs=(backend == "p2p" or (backend == "nccl" and n == 2)))
+
+
+MINI_PP_SCENARIO = {
+    "topology": {
+        "clusters": [{"nodes": 1, "nic": {"kind": "infiniband", "bandwidth_gbps": 200}},
+                     {"nodes": 1, "nic": {"kind": "roce", "bandwidth_gbps": 200}}],
+        "gpus_per_node": 2, "ethernet": {"bandwidth_gbps": 25}, "intra_node_bandwidth_gbps": 7200},
+    "model": {"layers": 6, "hidden": 256, "heads": 4, "seq_len": 512, "vocab": 1000,
+              "global_batch": 8, "micro_batch": 1},
+    "parallel": {"t": 1, "p": 2, "d": 2},
+    "partition": {"strategy": "self_adapting", "alpha": 1.05},
+    "cost": {"cluster_speeds_tflops": [197, 160]},
+    "notes": "4-GPU miniature of BASELINE config 4 (PP=2 x DP=2, two emulated NIC clusters)",
+}
+
+
+@pytest.mark.parametrize("backend,clip", [("p2p", 0.05), ("p2p", 0.0), ("nvls", 0.05)])
+def test_pp_dp_scenario_parity(oracle, tmp_path, backend, clip):
+    """Config 4 in miniature: per-stage DP rows from the reference-compatible plan,
+    stage gradient sets from the self-adapting partition, world-wide clip norm."""
+    if _ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    from paper_2312_03549_b200.gradsets import gpt_stage_tensors
+
+    scen = tmp_path / "mini_pp.json"
+    scen.write_text(json.dumps(MINI_PP_SCENARIO))
+    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+            "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+            str(ROOT / "tests" / "mp_worker_scenario.py"), "--scenario", str(scen), "--out", str(tmp_path),
+            "--clip", str(clip), "--backend", backend]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    metas = [json.loads((tmp_path / f"meta_r{q}.json").read_text()) for q in range(4)]
+    assert [m["stage"] for m in metas] == [1, 1, 2, 2]
+    assert [tuple(m["dp_ranks"]) for m in metas] == [(0, 1), (0, 1), (2, 3), (2, 3)]
+    layers = [m["stage_layers"] for m in metas]
+    assert layers[0] + layers[2] == 6
+    for step in (1, 2):
+        dumps = [np.load(tmp_path / f"r{q}_s{step}.npz") for q in range(4)]
+        if clip:
+            ss = sum(oracle.sumsq_bf16(d["reduced"]) for d in dumps)
+            for d in dumps:
+                assert abs(float(d["norm"]) - np.sqrt(ss)) <= 1e-5 * np.sqrt(ss)
+                assert d["coef"] == dumps[0]["coef"]
+        for stage, ranks in ((1, (0, 1)), (2, (2, 3))):
+            m0 = metas[ranks[0]]
+            first = 0 if stage == 1 else layers[0]
+            gs = gpt_stage_tensors(m0["stage_layers"], 256, 1000, stage=stage, pipeline=2, first_layer=first)
+            assert [[t.name, list(t.shape)] for t in gs.tensors] == m0["gradset"]
+            L = m0["layout"]
+            grads = [[u16(g).reshape(-1) for g in make_grads(gs, step, q, "cuda:0")] for q in ranks]
+            np.testing.assert_array_equal(dumps[ranks[0]]["params"], dumps[ranks[1]]["params"])
+            base = 0
+            for b in L["buckets"]:
+                packs = [oracle.pack([grads[k][i] for i in b["params"]], b["offsets"], b["numel"], 0.5)
+                         for k in range(2)]
+                sh = b["numel"] // 2
+                for k, q in enumerate(ranks):
+                    dev_red = dumps[q]["reduced"][base:base + sh]
+                    if backend == "p2p":
+                        np.testing.assert_array_equal(dev_red, oracle.reduce_scatter(packs, k, 2))
+                base += sh
+            for k, q in enumerate(ranks):
+                d = dumps[q]
+                master, mm, vv = d["pre_master"].copy(), d["pre_m"].copy(), d["pre_v"].copy()
+                oracle.adamw(master, mm, vv, d["reduced"], step, coef=float(d["coef"]) if clip else None)
+                np.testing.assert_array_equal(master.view(np.uint32), d["master"].view(np.uint32))
+                np.testing.assert_array_equal(vv.view(np.uint32), d["v"].view(np.uint32))
