@@ -28,13 +28,33 @@ from paper_2312_03549_b200.symm import SymmetricTensor  # noqa: E402
 
 
 def main():
+    import argparse as _ap
+
+    pre = _ap.ArgumentParser(add_help=False)
+    pre.add_argument("--sweep", action="store_true")
+    known, _ = pre.parse_known_args()
+    if known.sweep:
+        sizes = [(1 << 20) // 2 * (1 << k) for k in range(11)]      # 0.5M .. 512M elements
+        for n in sizes:
+            run_one(n, sweep=True)
+        return
+    run_one(None)
+
+
+def run_one(numel_override, sweep=False):
     ap = argparse.ArgumentParser()
     ap.add_argument("--numel", type=int, default=104_857_600)
+    ap.add_argument("--sweep", action="store_true",
+                    help="BASELINE config 5: bucket sizes 1 MB .. 1 GB (0.5M .. 512M bf16 elements)")
     ap.add_argument("--iters", type=int, default=20)
-    a = ap.parse_args()
+    a, _ = ap.parse_known_args()
+    if numel_override is not None:
+        a.numel = numel_override
+        a.iters = max(5, min(50, int(2e9 // (a.numel * 2))))
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
     dev = torch.device("cuda", rank)
     nat.load()
     N = a.numel - a.numel % (16 * world)
@@ -122,14 +142,22 @@ def main():
         nvl = 4 * n * (world - 1) if "fused" in name or "nccl" in name else 2 * n * (world - 1)
         if name == "adamw_local":
             nvl = 0
+        # nccl-tests convention for RS+AG over a bucket of N bf16 elements:
+        # busBW = (2 N bytes / t) * (d-1)/d per collective, two collectives
+        bus = (2 * 2 * N / (ms / 1e3)) * (world - 1) / world / 1e9 if ("fused" in name or "nccl" in name) else None
         out[name] = {"ms": round(ms, 4), "nvlink_GBps_per_dir": round(nvl / ms / 1e6, 1),
-                     "hbm_state_GBps": round(28 * n / ms / 1e6, 1)}
+                     "hbm_state_GBps": round(28 * n / ms / 1e6, 1),
+                     "busBW_GBps": round(bus, 1) if bus else None}
     if int(err.item()):
         out["error"] = int(err.item())
     if rank == 0:
-        print(json.dumps({"world": world, "numel": N, "shard": n, "results": out}, indent=1))
+        print(json.dumps({"world": world, "numel": N, "bucket_MB": round(2 * N / 2**20, 2), "shard": n,
+                          "results": out}, indent=None if sweep else 1), flush=True)
     comm.close()
-    dist.destroy_process_group()
+    del g, p, fl
+    torch.cuda.empty_cache()
+    if not sweep:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
