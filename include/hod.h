@@ -169,28 +169,35 @@ int hod_all_reduce_f32(float* buf, size_t n, void* comm, void* stream);
 #define HOD_P2P_RS 1
 #define HOD_P2P_ADAMW_AG 2
 
-typedef struct hod_p2p_bucket {
-  uint16_t* grad[HOD_P2P_MAX_RANKS];  /* rank q's bucket base; nvls: [0] = multicast base */
-  uint16_t* param[HOD_P2P_MAX_RANKS]; /* rank q's param-bucket base; nvls: [0] = multicast */
+#define HOD_P2P_MAX_SPAN 32
+
+/* A span of consecutive buckets (1..HOD_P2P_MAX_SPAN) handled by one launch. */
+typedef struct hod_p2p_span {
+  uint16_t* grad[HOD_P2P_MAX_RANKS];  /* rank q's flat grad-bucket buffer; nvls: [0] = multicast base */
+  uint16_t* param[HOD_P2P_MAX_RANKS]; /* rank q's flat param buffer; nvls: [0] = multicast base */
   uint32_t* flags[HOD_P2P_MAX_RANKS]; /* rank q's flag array: [slot][HOD_P2P_MAX_RANKS] u32 */
-  float* master;                      /* this rank's shard state, n elements each */
+  uint16_t* local_grad;   /* this rank's flat grad buffer: the reduced bf16 shard of bucket k is
+                             kept in place at bucket_start[k] + rank*shard_numel[k] (RS: out,
+                             ADAMW_AG: in, FUSED: only when keep_reduced) */
+  float* master;          /* this rank's state for the span's shards, back to back */
   float* exp_avg;
   float* exp_avg_sq;
-  uint16_t* reduced_out;  /* local bf16 reduced shard (RS: out, ADAMW_AG: in; FUSED: optional) */
-  float* partials;        /* RS: HOD_SUMSQ_PARTIALS sums of squares (optional) */
+  float* partials;        /* RS: HOD_SUMSQ_PARTIALS sums of squares for the span (optional) */
   const float* clip_coef; /* ADAMW_AG: device clip coefficient (optional) */
   uint32_t* err;          /* device error word (HOD_ETIMEOUT on a barrier timeout) */
-  int64_t shard_off;      /* element offset of this rank's shard inside the bucket */
-  int64_t n;              /* shard elements, multiple of 8 */
+  int64_t bucket_start[HOD_P2P_MAX_SPAN]; /* element offset of bucket k in the flat buffers */
+  int64_t shard_numel[HOD_P2P_MAX_SPAN];  /* bucket k's numel / d (multiple of 8) */
+  int n_buckets;
   int d;
   int rank;
   int nvls;
-  int slot;               /* barrier slot (bucket index) */
+  int keep_reduced;
+  int slot;               /* barrier slot (index of the span's first bucket) */
   uint32_t epoch;         /* monotonically increasing per step, > 0 */
   unsigned long long timeout_ns; /* barrier spin budget (0 = 20 s) */
-} hod_p2p_bucket;
+} hod_p2p_span;
 
-int hod_p2p_step(const hod_p2p_bucket* bucket, int mode, const hod_adamw_params* hp, void* stream);
+int hod_p2p_step(const hod_p2p_span* span, int mode, const hod_adamw_params* hp, void* stream);
 
 /* stand-alone cross-GPU barrier on `slot` (1 CTA): signal then wait for all d ranks */
 int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,

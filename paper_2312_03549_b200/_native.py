@@ -37,20 +37,23 @@ class PackEntry(ctypes.Structure):
 
 HOD_P2P_MAX_RANKS = 8
 HOD_P2P_FUSED, HOD_P2P_RS, HOD_P2P_ADAMW_AG = 0, 1, 2
+HOD_P2P_MAX_SPAN = 32
 
 
-class P2PBucket(ctypes.Structure):
-    """Mirror of hod_p2p_bucket (include/hod.h)."""
+class P2PSpan(ctypes.Structure):
+    """Mirror of hod_p2p_span (include/hod.h)."""
 
     _fields_ = [
         ("grad", ctypes.c_void_p * HOD_P2P_MAX_RANKS),
         ("param", ctypes.c_void_p * HOD_P2P_MAX_RANKS),
         ("flags", ctypes.c_void_p * HOD_P2P_MAX_RANKS),
+        ("local_grad", ctypes.c_void_p),
         ("master", ctypes.c_void_p), ("exp_avg", ctypes.c_void_p), ("exp_avg_sq", ctypes.c_void_p),
-        ("reduced_out", ctypes.c_void_p), ("partials", ctypes.c_void_p), ("clip_coef", ctypes.c_void_p),
-        ("err", ctypes.c_void_p),
-        ("shard_off", ctypes.c_int64), ("n", ctypes.c_int64),
-        ("d", ctypes.c_int), ("rank", ctypes.c_int), ("nvls", ctypes.c_int), ("slot", ctypes.c_int),
+        ("partials", ctypes.c_void_p), ("clip_coef", ctypes.c_void_p), ("err", ctypes.c_void_p),
+        ("bucket_start", ctypes.c_int64 * HOD_P2P_MAX_SPAN),
+        ("shard_numel", ctypes.c_int64 * HOD_P2P_MAX_SPAN),
+        ("n_buckets", ctypes.c_int), ("d", ctypes.c_int), ("rank", ctypes.c_int), ("nvls", ctypes.c_int),
+        ("keep_reduced", ctypes.c_int), ("slot", ctypes.c_int),
         ("epoch", ctypes.c_uint32), ("timeout_ns", ctypes.c_ulonglong),
     ]
 
@@ -98,7 +101,7 @@ def load(build_if_missing: bool = True):
         "hod_reduce_scatter_bf16": ([P, P, ctypes.c_size_t, P, P], I),
         "hod_all_gather_bf16": ([P, P, ctypes.c_size_t, P, P], I),
         "hod_all_reduce_f32": ([P, ctypes.c_size_t, P, P], I),
-        "hod_p2p_step": ([ctypes.POINTER(P2PBucket), I, ctypes.POINTER(AdamWParams), P], I),
+        "hod_p2p_step": ([ctypes.POINTER(P2PSpan), I, ctypes.POINTER(AdamWParams), P], I),
         "hod_p2p_barrier": ([P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, P], I),
         "hod_p2p_norm": ([P, I64, P, P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, F, P, P, P, P], I),
     }

@@ -121,7 +121,7 @@ class DistributedOptimizer:
                  norm_ranks=None, grad_scale: float | None = None, backend: str = "auto",
                  device=None, param_align: int = 64, process_group=None, norm_group=None,
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
-                 sm_budget: int | None = None):
+                 sm_budget: int | None = None, span_numel: int = 128 * 2**20):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -149,6 +149,10 @@ class DistributedOptimizer:
         # CTAs per launch while backward still runs (None = whole GPU); the last
         # bucket and the post-backward phase always get the whole GPU
         self.sm_budget = sm_budget
+        # p2p/nvls: consecutive packed buckets are coalesced into one fused
+        # launch until the span holds >= span_numel elements (1 = per bucket)
+        self.span_numel = int(span_numel)
+        self._pending_span: list[int] = []
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
 
@@ -268,7 +272,12 @@ class DistributedOptimizer:
         self._pending_grads = [dict() for _ in range(nb)]
         self._launched = [False] * nb
         self._deferred_ag = []
+        self._pending_span = []
         self._ev_start.record(torch.cuda.current_stream(self.device))
+        if self.clip is not None and self.backend in ("p2p", "nvls"):
+            # span starts (hence the partial slots written) may differ between steps
+            with torch.cuda.stream(self.s_comm):
+                self._partials.zero_()
 
     def grad_ready(self, param_index: int, grad: torch.Tensor) -> None:
         """Backward produced ``grad`` for parameter ``param_index`` (call from a
@@ -419,13 +428,7 @@ class DistributedOptimizer:
         self._launched[bi] = True
 
         if self.backend in ("p2p", "nvls"):
-            self.s_comm.wait_event(self._ev_packed[bi])
-            shard_ptr, _ = self._grad_shard(b)
-            if self.clip is None:
-                self._p2p(bi, nat.HOD_P2P_FUSED, reduced_out=shard_ptr if self.keep_reduced else None)
-            else:
-                part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * bi
-                self._p2p(bi, nat.HOD_P2P_RS, reduced_out=shard_ptr, partials=part)
+            self._queue_p2p(bi)
             return
 
         reduced = self._ev_packed[bi]
@@ -482,45 +485,84 @@ class DistributedOptimizer:
             arr[q] = sym.peer(q)
         return arr
 
-    def _p2p(self, bi: int, mode: int, reduced_out=None, partials=None, coef_ptr=None) -> None:
-        b = self.layout.buckets[bi]
-        d, n = self.dp, b.numel // self.dp
-        off = self._shard_off[bi]
-        bk = nat.P2PBucket()
+    def _p2p(self, bis, mode: int, partials=None, coef_ptr=None) -> None:
+        """One fused launch over the consecutive buckets ``bis`` (a span)."""
+        L = self.layout
+        d = self.dp
+        sp = nat.P2PSpan()
         if self.backend == "nvls":
-            bk.grad[0] = self._sym_grad.multicast(2 * b.start)
-            bk.param[0] = self._sym_param.multicast(2 * b.start)
+            sp.grad[0] = self._sym_grad.multicast()
+            sp.param[0] = self._sym_param.multicast()
         else:
             for q in range(d):
-                bk.grad[q] = self._sym_grad.peer(q, 2 * b.start)
-                bk.param[q] = self._sym_param.peer(q, 2 * b.start)
+                sp.grad[q] = self._sym_grad.peer(q)
+                sp.param[q] = self._sym_param.peer(q)
         for q in range(d):
-            bk.flags[q] = self._sym_flags.peer(q)
-        bk.master = _ptr(self.master) + 4 * off
-        bk.exp_avg = _ptr(self.exp_avg) + 4 * off
-        bk.exp_avg_sq = _ptr(self.exp_avg_sq) + 4 * off
-        bk.reduced_out = reduced_out
-        bk.partials = partials
-        bk.clip_coef = coef_ptr
-        bk.err = _ptr(self._err)
-        bk.shard_off = self.shard_index * n
-        bk.n = n
-        bk.d, bk.rank, bk.nvls = d, self.shard_index, int(self.backend == "nvls")
-        bk.slot, bk.epoch, bk.timeout_ns = bi, self.step_count, self.timeout_ns
+            sp.flags[q] = self._sym_flags.peer(q)
+        off = self._shard_off[bis[0]]
+        sp.local_grad = _ptr(self.grad_buffer)
+        sp.master = _ptr(self.master) + 4 * off
+        sp.exp_avg = _ptr(self.exp_avg) + 4 * off
+        sp.exp_avg_sq = _ptr(self.exp_avg_sq) + 4 * off
+        sp.partials = partials
+        sp.clip_coef = coef_ptr
+        sp.err = _ptr(self._err)
+        n_total = 0
+        for k, bi in enumerate(bis):
+            b = L.buckets[bi]
+            sp.bucket_start[k] = b.start
+            sp.shard_numel[k] = b.numel // d
+            n_total += b.numel // d
+        sp.n_buckets = len(bis)
+        sp.d, sp.rank, sp.nvls = d, self.shard_index, int(self.backend == "nvls")
+        sp.keep_reduced = int(self.keep_reduced)
+        sp.slot, sp.epoch, sp.timeout_ns = bis[0], self.step_count, self.timeout_ns
         hp = self._hp()
         name = {nat.HOD_P2P_FUSED: "fused", nat.HOD_P2P_RS: "rs", nat.HOD_P2P_ADAMW_AG: "adamw_ag"}[mode]
         # algorithmic bytes per launch: local HBM (state 24 B + own param 2 B +
         # own grad 2 B per owned element) — NVLink bytes are reported separately
-        nbytes = {"fused": 28 * n, "rs": 2 * d * n + 2 * n, "adamw_ag": 28 * n}[name]
+        nbytes = {"fused": 28 * n_total, "rs": 2 * d * n_total + 2 * n_total, "adamw_ag": 28 * n_total}[name]
         t0 = self._timed_event(self.s_comm)
-        nat.call("hod_p2p_step", ctypes.byref(bk), mode, ctypes.byref(hp), nat.stream_ptr(self.s_comm))
+        nat.call("hod_p2p_step", ctypes.byref(sp), mode, ctypes.byref(hp), nat.stream_ptr(self.s_comm))
         self._timed_close(name, t0, self.s_comm, nbytes)
+
+    def _spans(self, bis):
+        """Split consecutive bucket ids into spans of >= span_numel elements
+        (at most HOD_P2P_MAX_SPAN buckets each)."""
+        out, cur, acc = [], [], 0
+        for bi in bis:
+            cur.append(bi)
+            acc += self.layout.buckets[bi].numel
+            if acc >= self.span_numel or len(cur) == nat.HOD_P2P_MAX_SPAN:
+                out.append(cur)
+                cur, acc = [], 0
+        if cur:
+            out.append(cur)
+        return out
+
+    def _queue_p2p(self, bi: int, final: bool = False) -> None:
+        """Bucket bi is packed: extend the pending span, launch it when full."""
+        if bi is not None:
+            self._pending_span.append(bi)
+        pend = self._pending_span
+        full = (sum(self.layout.buckets[x].numel for x in pend) >= self.span_numel
+                or len(pend) == nat.HOD_P2P_MAX_SPAN)
+        if pend and (full or final):
+            self._pending_span = []
+            # the pack stream is in order: the span's last pack implies the others
+            self.s_comm.wait_event(self._ev_packed[pend[-1]])
+            if self.clip is None:
+                self._p2p(pend, nat.HOD_P2P_FUSED)
+            else:
+                part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * pend[0]
+                self._p2p(pend, nat.HOD_P2P_RS, partials=part)
 
     def _p2p_finish(self) -> None:
         nb = len(self.layout.buckets)
         s = self.s_comm
+        self._queue_p2p(None, final=True)
         if self.clip is not None:
-            if self.norm_ranks == (self.group.global_rank,) or len(self.norm_ranks) == 1:
+            if len(self.norm_ranks) == 1:
                 nat.call("hod_sum_partials", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS,
                          _ptr(self._sumsq), nat.stream_ptr(s))
                 nat.call("hod_clip_coef", _ptr(self._sumsq), ctypes.c_float(self.clip),
@@ -532,9 +574,8 @@ class DistributedOptimizer:
                          self._norm_d, self._norm_rank, 0, self.step_count, self.timeout_ns,
                          _ptr(self._err), ctypes.c_float(self.clip), _ptr(self._coef), _ptr(self._norm),
                          _ptr(self._sumsq), nat.stream_ptr(s))
-            for bi, b in enumerate(self.layout.buckets):
-                shard_ptr, _ = self._grad_shard(b)
-                self._p2p(bi, nat.HOD_P2P_ADAMW_AG, reduced_out=shard_ptr, coef_ptr=_ptr(self._coef))
+            for span in self._spans(range(nb)):
+                self._p2p(span, nat.HOD_P2P_ADAMW_AG, coef_ptr=_ptr(self._coef))
         # end-of-step barrier: every rank's param stores (and reads of our
         # buckets) are complete before anyone uses the params or repacks
         nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,

@@ -75,3 +75,36 @@ def test_built_for_sm100a_only():
         pytest.skip("cuobjdump unavailable")
     archs = set(re.findall(r"sm_(\d+a?)", out.stdout))
     assert archs == {"100a"}, out.stdout
+
+
+def test_struct_layouts_match_c(tmp_path):
+    """ctypes mirrors of the ABI structs have the C sizes and field offsets."""
+    import shutil
+    import subprocess
+
+    from paper_2312_03549_b200 import _native as nat
+
+    gxx = shutil.which("g++") or "/usr/bin/g++"
+    fields = {"hod_p2p_span": (nat.P2PSpan, ["local_grad", "master", "partials", "err", "bucket_start",
+                                             "shard_numel", "n_buckets", "keep_reduced", "slot",
+                                             "epoch", "timeout_ns"]),
+              "hod_pack_entry": (nat.PackEntry, ["src", "numel", "dst_offset"]),
+              "hod_adamw_params": (nat.AdamWParams, ["lr", "weight_decay", "step"])}
+    lines = ['#include <cstdio>', '#include <cstddef>', '#include "hod.h"', "int main() {"]
+    for cname, (_, names) in fields.items():
+        lines.append(f'  printf("%zu\\n", sizeof({cname}));')
+        for f in names:
+            lines.append(f'  printf("%zu\\n", offsetof({cname}, {f}));')
+    lines.append("}")
+    src = tmp_path / "layout.cpp"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    r = subprocess.run([gxx, f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], capture_output=True, text=True)
+    if r.returncode != 0:
+        pytest.skip(f"no C++ compiler: {r.stderr[:200]}")
+    got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = []
+    for _, (cls, names) in fields.items():
+        want.append(ctypes.sizeof(cls))
+        want += [getattr(cls, f).offset for f in names]
+    assert got == want

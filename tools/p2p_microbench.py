@@ -77,31 +77,33 @@ def run_one(numel_override, sweep=False):
     epoch = [0]
 
     def bucket(nvls):
-        bk = nat.P2PBucket()
+        sp = nat.P2PSpan()
         if nvls:
-            bk.grad[0], bk.param[0] = g.multicast(), p.multicast()
+            sp.grad[0], sp.param[0] = g.multicast(), p.multicast()
         else:
             for q in range(world):
-                bk.grad[q], bk.param[q] = g.peer(q), p.peer(q)
+                sp.grad[q], sp.param[q] = g.peer(q), p.peer(q)
         for q in range(world):
-            bk.flags[q] = fl.peer(q)
-        bk.master, bk.exp_avg, bk.exp_avg_sq = master.data_ptr(), m.data_ptr(), v.data_ptr()
-        bk.err = err.data_ptr()
-        bk.shard_off, bk.n, bk.d, bk.rank, bk.nvls = rank * n, n, world, rank, int(nvls)
-        bk.slot, bk.timeout_ns = 0, 10_000_000_000
-        return bk
+            sp.flags[q] = fl.peer(q)
+        sp.local_grad = g.tensor.data_ptr()
+        sp.master, sp.exp_avg, sp.exp_avg_sq = master.data_ptr(), m.data_ptr(), v.data_ptr()
+        sp.err = err.data_ptr()
+        sp.bucket_start[0], sp.shard_numel[0], sp.n_buckets = 0, n, 1
+        sp.d, sp.rank, sp.nvls = world, rank, int(nvls)
+        sp.slot, sp.timeout_ns = 0, 10_000_000_000
+        return sp
 
     hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, 1)
 
     def run_mode(mode, nvls):
-        bk = bucket(nvls)
+        sp = bucket(nvls)
         epoch[0] += 1
-        bk.epoch = epoch[0]
+        sp.epoch = epoch[0]
         if mode == nat.HOD_P2P_RS:
-            bk.reduced_out, bk.partials = red.data_ptr(), parts.data_ptr()
+            sp.partials = parts.data_ptr()
         if mode == nat.HOD_P2P_ADAMW_AG:
-            bk.reduced_out, bk.clip_coef = red.data_ptr(), coef.data_ptr()
-        nat.call("hod_p2p_step", ctypes.byref(bk), mode, ctypes.byref(hp), s.cuda_stream)
+            sp.clip_coef = coef.data_ptr()
+        nat.call("hod_p2p_step", ctypes.byref(sp), mode, ctypes.byref(hp), s.cuda_stream)
 
     comm = NcclComm(tuple(range(world)), rank, "bench")
 
