@@ -260,7 +260,8 @@ def run_ours(args) -> None:
         gs = sr.gradset
         clip = 1.0 if args.clip is None else (None if args.clip <= 0 else args.clip)
         p0 = init_params(gs, dev)
-        opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=clip, backend=args.backend)
+        opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=clip, backend=args.backend,
+                             span_numel=args.span_numel)
         stage_params = {sr.placement.stage: gs.total}
         gathered = [None] * world
         import torch.distributed as dist
@@ -277,7 +278,7 @@ def run_ours(args) -> None:
         p0 = init_params(gs, dev)
         group = DPGroup(tuple(range(world)), rank)
         opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group,
-                                   backend=args.backend)
+                                   backend=args.backend, span_numel=args.span_numel)
     del p0
     torch.cuda.empty_cache()
     grads = make_grads(gs, 1, rank, dev, dtype=gdtype)
@@ -416,6 +417,8 @@ def main():
                     help="scenario JSON (reference schema) for a PP x DP run, e.g. "
                          "scenarios/gpt13b_pp2_dp4_hybrid.json (BASELINE config 4, 8 GPUs)")
     ap.add_argument("--bucket-size", type=int, default=25_000_000)
+    ap.add_argument("--span-numel", type=int, default=128 * 2**20,
+                    help="p2p/nvls: coalesce packed buckets into fused launches of >= this many elements")
     ap.add_argument("--backend", default="auto")
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")
     ap.add_argument("--no-e2e", action="store_true")
