@@ -151,30 +151,24 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
     while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;  // CTA-uniform
     const bool inside = e < t.n && t.off[e] <= a && b <= t.off[e] + t.numel[e];
     if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kFusedTile) {
-      float g[8];
-      load8<SrcT>(t.src[e], a - t.off[e] + static_cast<int64_t>(threadIdx.x) * 8, g);
+      // warp w owns elements [a + 256w, a + 256w + 256): lane quads at 4l and 128 + 4l
+      const int64_t e0 = a + (threadIdx.x >> 5) * kChunk + (threadIdx.x & 31) * 4;
+      float g[8], pf[8], mf[8], vf[8];
+      if constexpr (sizeof(SrcT) == 2) ld_bf16_quads(static_cast<const uint16_t*>(t.src[e]), e0 - t.off[e], g);
+      else ld_f32_quads(static_cast<const float*>(t.src[e]), e0 - t.off[e], g);
+      ld_f32_quads(p, e0, pf);
+      ld_f32_quads(m, e0, mf);
+      ld_f32_quads(v, e0, vf);
 #pragma unroll
       for (int k = 0; k < 8; ++k) {
         g[k] = bf16_to_f32(f32_to_bf16(__fmul_rn(g[k], scale)));
         if (kClip) g[k] = __fmul_rn(g[k], coef);
+        adamw_elem(pf[k], mf[k], vf[k], g[k], c);
       }
-      const int64_t iv = a / 8 + threadIdx.x;
-      float4* p4 = reinterpret_cast<float4*>(p) + 2 * iv;
-      float4* m4 = reinterpret_cast<float4*>(m) + 2 * iv;
-      float4* v4 = reinterpret_cast<float4*>(v) + 2 * iv;
-      float4 pa = p4[0], pb = p4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
-      float pf[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-      float mf[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-      float vf[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
-#pragma unroll
-      for (int k = 0; k < 8; ++k) adamw_elem(pf[k], mf[k], vf[k], g[k], c);
-      p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
-      p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
-      m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
-      m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
-      v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
-      v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
-      reinterpret_cast<uint4*>(out)[iv] = pack8(pf);
+      st_f32_quads(p, e0, pf);
+      st_f32_quads(m, e0, mf);
+      st_f32_quads(v, e0, vf);
+      st_bf16_quads(out, e0, pf);
     } else {
       int ei = e;
       for (int64_t i = a + threadIdx.x; i < b; i += kThreads) {
@@ -200,39 +194,28 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
 template <typename GradT, bool kClip>
 __global__ void __launch_bounds__(kThreads) adamw_vec_kernel(
     float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-    const GradT* __restrict__ g, uint16_t* __restrict__ out, int64_t n_vec,
+    const GradT* __restrict__ g, uint16_t* __restrict__ out, int64_t n_chunks,
     const AdamWConsts c, const float* __restrict__ coef_ptr) {
   const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
-  for (int64_t iv = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; iv < n_vec; iv += stride) {
-    float gf[8];
-    if constexpr (sizeof(GradT) == 2) {
-      unpack8(__ldg(reinterpret_cast<const uint4*>(g) + iv), gf);
-    } else {
-      const float4 a = __ldg(reinterpret_cast<const float4*>(g) + 2 * iv);
-      const float4 b = __ldg(reinterpret_cast<const float4*>(g) + 2 * iv + 1);
-      gf[0] = a.x; gf[1] = a.y; gf[2] = a.z; gf[3] = a.w;
-      gf[4] = b.x; gf[5] = b.y; gf[6] = b.z; gf[7] = b.w;
-    }
-    float4* p4 = reinterpret_cast<float4*>(p) + 2 * iv;
-    float4* m4 = reinterpret_cast<float4*>(m) + 2 * iv;
-    float4* v4 = reinterpret_cast<float4*>(v) + 2 * iv;
-    float4 pa = p4[0], pb = p4[1], ma = m4[0], mb = m4[1], va = v4[0], vb = v4[1];
-    float pf[8] = {pa.x, pa.y, pa.z, pa.w, pb.x, pb.y, pb.z, pb.w};
-    float mf[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-    float vf[8] = {va.x, va.y, va.z, va.w, vb.x, vb.y, vb.z, vb.w};
+  const int lane = threadIdx.x & 31;
+  const int64_t n_warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+  for (int64_t ch = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; ch < n_chunks; ch += n_warps) {
+    const int64_t e0 = ch * kChunk + lane * 4;
+    float gf[8], pf[8], mf[8], vf[8];
+    if constexpr (sizeof(GradT) == 2) ld_bf16_quads(reinterpret_cast<const uint16_t*>(g), e0, gf);
+    else ld_f32_quads(reinterpret_cast<const float*>(g), e0, gf);
+    ld_f32_quads(p, e0, pf);
+    ld_f32_quads(m, e0, mf);
+    ld_f32_quads(v, e0, vf);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float gk = kClip ? __fmul_rn(gf[k], coef) : gf[k];
       adamw_elem(pf[k], mf[k], vf[k], gk, c);
     }
-    p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
-    p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
-    m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
-    m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
-    v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
-    v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
-    reinterpret_cast<uint4*>(out)[iv] = pack8(pf);
+    st_f32_quads(p, e0, pf);
+    st_f32_quads(m, e0, mf);
+    st_f32_quads(v, e0, vf);
+    st_bf16_quads(out, e0, pf);
   }
 }
 
@@ -269,16 +252,16 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
                    aligned16(grad) && aligned16(param);
   int64_t done = 0;
   if (vec) {
-    const int64_t n_vec = n / 8;
+    const int64_t n_vec = n / kChunk;   // whole 256-element warp chunks
     if (n_vec > 0) {
-      const int grid = grid_for(n_vec, kThreads);
+      const int grid = grid_for(n_vec * 32, kThreads);
       count_launch(1);
       if (clip_coef)
         adamw_vec_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef);
       else
         adamw_vec_kernel<GradT, false><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, nullptr);
     }
-    done = n_vec * 8;
+    done = n_vec * kChunk;
   }
   if (done < n) {
     const int grid = grid_for(n - done, kThreads);
