@@ -11,9 +11,9 @@
 //   FUSED (no clip): ONE kernel per span —
 //       cross-GPU arrival barrier (peer flag stores, acquire spin);
 //       reduce-scatter: rank r sums shard r of every bucket of every peer
-//         p2p : d 16-byte P2P loads, fp32 sum in rank order 0..d-1, one RNE
-//               rounding to bf16  -> bit-exact with oracle_rs_sum;
-//         nvls: one multimem.ld_reduce.add.acc::f32 per 8 elements (the
+//         p2p : d 8-byte P2P loads per quad, fp32 sum in rank order 0..d-1, one
+//               RNE rounding to bf16  -> bit-exact with oracle_rs_sum;
+//         nvls: one multimem.ld_reduce.add.acc::f32 per 4 elements (the
 //               switch reduces: ingress per GPU drops from 2P(d-1)/d to 2P/d);
 //       AdamW on the fp32 master/m/v shard (local HBM, 24 B/elem);
 //       all-gather: the bf16 param vector is stored to every peer's param
@@ -64,7 +64,7 @@ struct SpanArgs {
   float* partials;          // optional: HOD_SUMSQ_PARTIALS per-CTA sums of squares
   const float* coef;        // optional clip coefficient (device)
   int64_t own_off[kMaxSpan];     // element offset of this rank's shard of bucket k
-  int64_t item_end[kMaxSpan];    // prefix (inclusive) of shard items (8 elements) over the span
+  int64_t elem_end[kMaxSpan];    // prefix (inclusive) of shard elements over the span
   int n_buckets;
   int d;
   int keep_reduced;
@@ -111,23 +111,6 @@ __device__ bool cross_gpu_barrier(const BarrierArgs& b, int d, int rank) {
   return timed_out == 0;
 }
 
-__device__ __forceinline__ uint4 ld_reduce_bf16x8(const uint16_t* mc) {
-  uint4 r;
-  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(mc)
-               : "memory");
-  return r;
-}
-
-__device__ __forceinline__ void st_multicast16(uint16_t* mc, const uint4& q) {
-  // .v4 multimem stores take a float vector; the 16 bytes are moved bit-for-bit
-  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc),
-               "f"(__uint_as_float(q.x)), "f"(__uint_as_float(q.y)), "f"(__uint_as_float(q.z)),
-               "f"(__uint_as_float(q.w))
-               : "memory");
-}
-
 __device__ __forceinline__ float block_sum_f(float x) {
   __shared__ float part[kThreads / 32];
 #pragma unroll
@@ -140,111 +123,131 @@ __device__ __forceinline__ float block_sum_f(float x) {
   return s;
 }
 
-// One thread's 8-element work item, split into a load phase and a compute /
-// store phase so that U items can have all their loads in flight at once.
+__device__ __forceinline__ uint2 ld_reduce_bf16x4(const uint16_t* mc) {
+  uint2 r;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v2.bf16x2 {%0, %1}, [%2];"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(mc)
+               : "memory");
+  return r;
+}
+
+__device__ __forceinline__ void st_multicast8(uint16_t* mc, const uint2& q) {
+  asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(mc),
+               "f"(__uint_as_float(q.x)), "f"(__uint_as_float(q.y))
+               : "memory");
+}
+
+// One thread's work item: the two quads (4 elements each) it owns in a
+// 256-element warp chunk of the span (lane*4 and 128 + lane*4, see kChunk in
+// hod_common.cuh), so every warp-wide access is a fully used contiguous span.
+// Quads never straddle buckets (shards are multiples of 16 elements); each
+// quad is located on its own.  Split into a load phase and a compute/store
+// phase so U items can have all their loads in flight at once.
 template <int D, bool kNVLS>
 struct Item {
   static constexpr int kRaw = kNVLS ? 1 : (D > 0 ? D : kMaxRanks);
-  uint4 raw[kRaw];     // peers' bucket vectors (p2p), the switch-reduced vector (nvls),
-                       // or the local reduced shard (mode 2, raw[0])
-  float4 st[6];        // master, m, v (two float4 each)
-  int64_t e;           // element offset in the flat buffers
-  int64_t s;           // element offset in the span's state
+  uint2 raw[2][kRaw];  // per quad: peers' bucket vectors (p2p), the switch-reduced
+                       // vector (nvls) or the local reduced shard (mode 2, raw[h][0])
+  float4 st[2][3];     // per quad: master, m, v
+  int64_t e[2];        // element offset in the flat buffers
+  int64_t s[2];        // element offset in the span's state
+  bool ok[2];
 };
 
-// Map a span item index to (flat element offset, state offset); `k` is the
-// caller's monotonically advancing bucket cursor.
-__device__ __forceinline__ void locate(const SpanArgs& a, int64_t iv, int& k, int64_t& e, int64_t& s) {
-  while (k < a.n_buckets - 1 && iv >= a.item_end[k]) ++k;
-  const int64_t first = k ? a.item_end[k - 1] : 0;
-  e = a.own_off[k] + (iv - first) * 8;
-  s = iv * 8;
+// Locate the quad starting at span element f; `k` is the caller's
+// monotonically advancing bucket cursor.
+__device__ __forceinline__ bool locate(const SpanArgs& a, int64_t f, int& k, int64_t& e, int64_t& s) {
+  if (f >= a.elem_end[a.n_buckets - 1]) return false;
+  while (k < a.n_buckets - 1 && f >= a.elem_end[k]) ++k;
+  const int64_t first = k ? a.elem_end[k - 1] : 0;
+  e = a.own_off[k] + (f - first);
+  s = f;
+  return true;
 }
 
 template <int D, bool kNVLS, int kMode>
 __device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kNVLS>& it) {
-  const int64_t e = it.e;
-  if (kMode == 2) {
-    it.raw[0] = *reinterpret_cast<const uint4*>(a.local_grad + e);
-  } else if constexpr (kNVLS) {
-    it.raw[0] = ld_reduce_bf16x8(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e);
-  } else {
-    const int dd = D > 0 ? D : a.d;
 #pragma unroll
-    for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q)
-      if (q < dd) it.raw[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
-  }
-  if (kMode != 1) {
-    const float4* p4 = reinterpret_cast<const float4*>(a.master + it.s);
-    const float4* m4 = reinterpret_cast<const float4*>(a.m + it.s);
-    const float4* v4 = reinterpret_cast<const float4*>(a.v + it.s);
-    it.st[0] = p4[0]; it.st[1] = p4[1];
-    it.st[2] = m4[0]; it.st[3] = m4[1];
-    it.st[4] = v4[0]; it.st[5] = v4[1];
+  for (int h = 0; h < 2; ++h) {
+    if (!it.ok[h]) continue;
+    const int64_t e = it.e[h];
+    if (kMode == 2) {
+      it.raw[h][0] = *reinterpret_cast<const uint2*>(a.local_grad + e);
+    } else if constexpr (kNVLS) {
+      it.raw[h][0] = ld_reduce_bf16x4(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e);
+    } else {
+      const int dd = D > 0 ? D : a.d;
+#pragma unroll
+      for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q)
+        if (q < dd) it.raw[h][q] = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
+    }
+    if (kMode != 1) {
+      it.st[h][0] = *reinterpret_cast<const float4*>(a.master + it.s[h]);
+      it.st[h][1] = *reinterpret_cast<const float4*>(a.m + it.s[h]);
+      it.st[h][2] = *reinterpret_cast<const float4*>(a.v + it.s[h]);
+    }
   }
 }
 
 template <int D, bool kNVLS>
-__device__ __forceinline__ void gather_store8(const SpanArgs& a, int64_t e, const uint4& q8) {
+__device__ __forceinline__ void gather_store4(const SpanArgs& a, int64_t e, const uint2& q4) {
   if constexpr (kNVLS) {
-    st_multicast16(reinterpret_cast<uint16_t*>(a.param.p[0]) + e, q8);
+    st_multicast8(reinterpret_cast<uint16_t*>(a.param.p[0]) + e, q4);
   } else {
     const int dd = D > 0 ? D : a.d;
 #pragma unroll
     for (int q = 0; q < (D > 0 ? D : kMaxRanks); ++q)
-      if (q < dd) *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(a.param.p[q]) + e) = q8;
+      if (q < dd) *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(a.param.p[q]) + e) = q4;
   }
 }
 
 template <int D, bool kNVLS, int kMode>
 __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kNVLS>& it,
                                             const AdamWConsts& c, float coef, float& ss) {
-  float g[8];
-  if (kMode == 2 || kNVLS) {
-    unpack8(it.raw[0], g);
-  } else {
-    const int dd = D > 0 ? D : a.d;
-    float acc[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) acc[k] = 0.0f;
+  for (int h = 0; h < 2; ++h) {
+    if (!it.ok[h]) continue;
+    float g[4];
+    if (kMode == 2 || kNVLS) {
+      unpack4(it.raw[h][0], g);
+    } else {
+      const int dd = D > 0 ? D : a.d;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q) {
-      if (q < dd) {
-        float f[8];
-        unpack8(it.raw[q], f);
+      for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q) {
+        if (q < dd) {
+          float f[4];
+          unpack4(it.raw[h][q], f);
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+          for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) g[k] = bf16_to_f32(f32_to_bf16(acc[k]));
+    }
+    if (kMode != 2) {
+      if (kMode == 1 || a.keep_reduced) *reinterpret_cast<uint2*>(a.local_grad + it.e[h]) = pack4(g);
+      if (kMode == 1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) ss = __fadd_rn(ss, __fmul_rn(g[k], g[k]));
+        continue;
       }
     }
+    const float4 P = it.st[h][0], M = it.st[h][1], V = it.st[h][2];
+    float pf[4] = {P.x, P.y, P.z, P.w};
+    float mf[4] = {M.x, M.y, M.z, M.w};
+    float vf[4] = {V.x, V.y, V.z, V.w};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) g[k] = bf16_to_f32(f32_to_bf16(acc[k]));
-  }
-  if (kMode != 2) {
-    if (kMode == 1 || a.keep_reduced) *reinterpret_cast<uint4*>(a.local_grad + it.e) = pack8(g);
-    if (kMode == 1) {
-#pragma unroll
-      for (int k = 0; k < 8; ++k) ss = __fadd_rn(ss, __fmul_rn(g[k], g[k]));
-      return;
+    for (int k = 0; k < 4; ++k) {
+      const float gk = (kMode == 2 && a.coef) ? __fmul_rn(g[k], coef) : g[k];
+      adamw_elem(pf[k], mf[k], vf[k], gk, c);
     }
+    *reinterpret_cast<float4*>(a.master + it.s[h]) = make_float4(pf[0], pf[1], pf[2], pf[3]);
+    *reinterpret_cast<float4*>(a.m + it.s[h]) = make_float4(mf[0], mf[1], mf[2], mf[3]);
+    *reinterpret_cast<float4*>(a.v + it.s[h]) = make_float4(vf[0], vf[1], vf[2], vf[3]);
+    gather_store4<D, kNVLS>(a, it.e[h], pack4(pf));
   }
-  float pf[8] = {it.st[0].x, it.st[0].y, it.st[0].z, it.st[0].w, it.st[1].x, it.st[1].y, it.st[1].z, it.st[1].w};
-  float mf[8] = {it.st[2].x, it.st[2].y, it.st[2].z, it.st[2].w, it.st[3].x, it.st[3].y, it.st[3].z, it.st[3].w};
-  float vf[8] = {it.st[4].x, it.st[4].y, it.st[4].z, it.st[4].w, it.st[5].x, it.st[5].y, it.st[5].z, it.st[5].w};
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    const float gk = (kMode == 2 && a.coef) ? __fmul_rn(g[k], coef) : g[k];
-    adamw_elem(pf[k], mf[k], vf[k], gk, c);
-  }
-  float4* p4 = reinterpret_cast<float4*>(a.master + it.s);
-  float4* m4 = reinterpret_cast<float4*>(a.m + it.s);
-  float4* v4 = reinterpret_cast<float4*>(a.v + it.s);
-  p4[0] = make_float4(pf[0], pf[1], pf[2], pf[3]);
-  p4[1] = make_float4(pf[4], pf[5], pf[6], pf[7]);
-  m4[0] = make_float4(mf[0], mf[1], mf[2], mf[3]);
-  m4[1] = make_float4(mf[4], mf[5], mf[6], mf[7]);
-  v4[0] = make_float4(vf[0], vf[1], vf[2], vf[3]);
-  v4[1] = make_float4(vf[4], vf[5], vf[6], vf[7]);
-  gather_store8<D, kNVLS>(a, it.e, pack8(pf));
 }
 
 // kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+in-place reduced shard, partials),
@@ -258,26 +261,26 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constan
     if (!cross_gpu_barrier(b, a.d, rank)) return;
   }
   const float coef = (kMode == 2 && a.coef) ? __ldg(a.coef) : 1.0f;
-  const int64_t n_items = a.item_end[a.n_buckets - 1];
-  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  const int64_t n_chunks = (a.elem_end[a.n_buckets - 1] + kChunk - 1) / kChunk;
+  const int64_t n_warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+  const int lane = threadIdx.x & 31;
   float ss = 0.0f;
   int cur[U];
 #pragma unroll
   for (int u = 0; u < U; ++u) cur[u] = 0;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; base < n_items;
-       base += stride * U) {
+  for (int64_t base = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; base < n_chunks;
+       base += n_warps * U) {
     Item<D, kNVLS> it[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int64_t iv = base + u * stride;
-      if (iv < n_items) {
-        locate(a, iv, cur[u], it[u].e, it[u].s);
-        load_item<D, kNVLS, kMode>(a, it[u]);
-      }
+      const int64_t ch = base + u * n_warps;
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        it[u].ok[h] = ch < n_chunks && locate(a, ch * kChunk + h * 128 + lane * 4, cur[u], it[u].e[h], it[u].s[h]);
+      load_item<D, kNVLS, kMode>(a, it[u]);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (base + u * stride < n_items) finish_item<D, kNVLS, kMode>(a, it[u], c, coef, ss);
+    for (int u = 0; u < U; ++u) finish_item<D, kNVLS, kMode>(a, it[u], c, coef, ss);
   }
   if (kMode == 1 && a.partials) {
     const float s = block_sum_f(ss);
@@ -393,7 +396,7 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
   if (!a->local_grad || (reinterpret_cast<uintptr_t>(a->local_grad) & 15)) {
     set_error("hod_p2p: local grad buffer null or misaligned"); return HOD_EALIGN;
   }
-  int64_t items = 0;
+  int64_t elems = 0;
   for (int k = 0; k < sp->n_buckets; ++k) {
     const int64_t n = sp->shard_numel[k];
     if (n < 8 || (n & 7) || sp->bucket_start[k] < 0 || (sp->bucket_start[k] & 7)) {
@@ -401,8 +404,8 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
       return HOD_EALIGN;
     }
     a->own_off[k] = sp->bucket_start[k] + static_cast<int64_t>(sp->rank) * n;
-    items += n / 8;
-    a->item_end[k] = items;
+    elems += n;
+    a->elem_end[k] = elems;
   }
   a->master = sp->master;
   a->m = sp->exp_avg;
@@ -430,9 +433,9 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
   if (mode != HOD_P2P_RS && (!hp || hp->step < 1)) { set_error("hod_p2p_step: bad hp/step"); return HOD_EINVAL; }
   if (mode != HOD_P2P_RS && (!a.master || !a.m || !a.v)) { set_error("hod_p2p_step: null state"); return HOD_EINVAL; }
   const AdamWConsts c = (mode != HOD_P2P_RS) ? fold_adamw(*hp) : AdamWConsts{};
-  const int64_t items = a.item_end[a.n_buckets - 1];
+  const int64_t chunks = (a.elem_end[a.n_buckets - 1] + kChunk - 1) / kChunk;
   // RS keeps a FIXED grid so its sum-of-squares partials are reproducible
-  const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(items, kThreads, 4);
+  const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(chunks * 32, kThreads, 4);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool nv = sp->nvls != 0;
   if (mode == HOD_P2P_FUSED) {

@@ -134,10 +134,12 @@ class DistributedOptimizer:
         self.grad_scale = (1.0 / self.dp) if grad_scale is None else float(grad_scale)
         auto = backend == "auto"
         if auto:
-            # measured choice (tools/p2p_microbench.py): P2P loads/stores
-            # up to d = 4; at d = 8 NVLS moves 18n instead of 28n bytes per
-            # direction per GPU (falls back to p2p when multicast is unavailable)
-            backend = "none" if self.dp == 1 else ("nvls" if self.dp >= 8 else "p2p")
+            # measured choice (tools/p2p_microbench.py, bench.py): P2P
+            # loads/stores at d = 2 (NVLS loops the own shard through the switch);
+            # NVLS from d = 4 (measured 6.61 vs 6.80 ms/step at d = 4), and at
+            # d = 8 it moves 18n instead of 28n bytes per direction per GPU
+            # (falls back to p2p when multicast is unavailable)
+            backend = "none" if self.dp == 1 else ("nvls" if self.dp >= 4 else "p2p")
         if backend not in BACKENDS:
             raise InfeasibleConfigError(f"unknown backend {backend!r} (choose from {BACKENDS})")
         if (backend == "none") != (self.dp == 1):
