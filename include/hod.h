@@ -129,6 +129,15 @@ int hod_adamw_bf16(float* master, float* exp_avg, float* exp_avg_sq,
                    const uint16_t* grad, uint16_t* param, int64_t n,
                    const hod_adamw_params* hp, const float* clip_coef, void* stream);
 
+/* Same update fed by the Tensor Memory Accelerator: 2048-element chunks are
+ * bulk-copied (cp.async.bulk) into a shared-memory ring by one producer thread
+ * per CTA and bulk-stored back, so `max_ctas` CTAs (0 = one per SM) stream at
+ * HBM speed from few threads — the SM-light variant for overlap with compute.
+ * Bit-identical to hod_adamw_bf16. */
+int hod_adamw_tma(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* grad,
+                  uint16_t* param, int64_t n, const hod_adamw_params* hp, const float* clip_coef,
+                  int max_ctas, void* stream);
+
 /* Same update reading an fp32 gradient (fp32 reduce-scatter parity mode). */
 int hod_adamw_f32(float* master, float* exp_avg, float* exp_avg_sq,
                   const float* grad, uint16_t* param, int64_t n,

@@ -122,8 +122,12 @@ __device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g
 // co-run with the backward GEMMs on a bounded slice of the SMs.
 int grid_limit();
 
+// HOD_CTAS_PER_SM (env) overrides the per-kernel CTAs-per-SM cap (tuning runs).
+int ctas_per_sm_override();
+
 inline int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 8) {
   int64_t need = (work_items + per_block - 1) / per_block;
+  if (ctas_per_sm_override() > 0) max_blocks_per_sm = ctas_per_sm_override();
   int64_t cap = static_cast<int64_t>(kSMs) * max_blocks_per_sm;
   if (grid_limit() > 0 && grid_limit() < cap) cap = grid_limit();
   if (need < 1) need = 1;

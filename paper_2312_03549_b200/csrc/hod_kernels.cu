@@ -7,6 +7,7 @@
 #include <math.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <atomic>
@@ -22,6 +23,14 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
 static thread_local int g_grid_limit = 0;
 int grid_limit() { return g_grid_limit; }
+
+int ctas_per_sm_override() {
+  static const int v = [] {
+    const char* e = getenv("HOD_CTAS_PER_SM");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -254,7 +263,8 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
   if (vec) {
     const int64_t n_vec = n / kChunk;   // whole 256-element warp chunks
     if (n_vec > 0) {
-      const int grid = grid_for(n_vec * 32, kThreads);
+      // 2 CTAs/SM measured best (6.3 TB/s vs 5.9 TB/s at 4-8/SM; tools/sweep_grid.sh)
+      const int grid = grid_for(n_vec * 32, kThreads, 2);
       count_launch(1);
       if (clip_coef)
         adamw_vec_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef);
@@ -408,7 +418,8 @@ int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket
     if (!aligned16(bucket + lo)) {
       set_error("hod_pack_bf16: window start %lld not 16-byte aligned", (long long)lo); return HOD_EALIGN;
     }
-    const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, 4);
+    // measured best: 8 CTAs/SM for bf16 sources, 3 for fp32 (tools/sweep_grid.sh)
+    const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, src_dtype == HOD_DTYPE_BF16 ? 8 : 3);
     count_launch(1);
     if (src_dtype == HOD_DTYPE_BF16)
       pack_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
@@ -432,7 +443,7 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return for_each_window("hod_pack_adamw", entries, n_entries, bucket_numel, src_dtype,
                          [&](const PackTable& t, int64_t lo, int64_t span) {
-    const int grid = grid_for((span + kFusedTile - 1) / kFusedTile, 1, 8);
+    const int grid = grid_for((span + kFusedTile - 1) / kFusedTile, 1, 3);  // measured best: 3/SM
     count_launch(1);
 #define HOD_PA_LAUNCH(T, CLIP) \
     pack_adamw_kernel<T, CLIP><<<grid, kThreads, 0, s>>>(t, span, scale, master + lo, exp_avg + lo, \
