@@ -104,7 +104,7 @@ def main():
     doc = {"round": a.round, "note": a.note, "kernels": {}}
     if a.launches:
         doc["launch_list"] = launches(Path(a.launches))
-    spec = {"adamw": (14, 14, 28), "pack": (2, 2, 4), "fused": (None, None, 28)}
+    spec = {"adamw": (14, 14, 28), "pack": (2, 2, 4), "pack_adamw": (14, 14, 28), "fused": (None, None, 28)}
     for item in a.rep:
         name, path = item.split("=", 1)
         rd, wr, alg = spec.get(name, (None, None, None))
