@@ -121,7 +121,8 @@ class DistributedOptimizer:
                  norm_ranks=None, grad_scale: float | None = None, backend: str = "auto",
                  device=None, param_align: int = 64, process_group=None, norm_group=None,
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
-                 sm_budget: int | None = None, span_numel: int = 128 * 2**20):
+                 sm_budget: int | None = None, span_numel: int = 128 * 2**20,
+                 param_barriers: bool = True):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -154,6 +155,10 @@ class DistributedOptimizer:
         # p2p/nvls: consecutive packed buckets are coalesced into one fused
         # launch until the span holds >= span_numel elements (1 = per bucket)
         self.span_numel = int(span_numel)
+        # p2p/nvls: a params-ready barrier after every span (enables per-bucket
+        # wait_params for a forward-overlapped all-gather) instead of a single
+        # end-of-step barrier
+        self.param_barriers = bool(param_barriers)
         self._pending_span: list[int] = []
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
@@ -174,7 +179,8 @@ class DistributedOptimizer:
             self._sym_grad = SymmetricTensor(total, _BF16, dev, pg)
             self._sym_param = SymmetricTensor(total, _BF16, dev, pg, zero=True)
             # barrier flags: slots 0..nb-1 per bucket, nb = end-of-step
-            self._sym_flags = SymmetricTensor((nb + 1) * nat.HOD_P2P_MAX_RANKS, torch.int32, dev, pg,
+            # barrier slots: [0, nb) span arrival, nb end of step, nb+1+b span done
+            self._sym_flags = SymmetricTensor((2 * nb + 1) * nat.HOD_P2P_MAX_RANKS, torch.int32, dev, pg,
                                               zero=True)
             if self._sym_grad.rank != self.shard_index:
                 raise InfeasibleConfigError("process group order differs from the DP row order")
@@ -291,8 +297,14 @@ class DistributedOptimizer:
         if len(pend) == len(b.slots):
             self._launch_bucket(slot.bucket)
 
-    def finish_step(self) -> StepReport:
-        """Launch whatever is left, run the clip barrier if needed, and return."""
+    def finish_step(self, wait: bool = True) -> StepReport:
+        """Launch whatever is left, run the clip barrier if needed, and return.
+
+        ``wait=False`` leaves the current stream free: the next forward then
+        calls ``wait_params(b)`` before it touches bucket b (p2p/nvls buckets
+        become ready span by span — in reverse bucket order after a clip norm,
+        i.e. first-layer parameters first), overlapping the all-gather with
+        the next forward."""
         L = self.layout
         for b in range(len(L.buckets)):
             if not self._launched[b]:
@@ -305,9 +317,12 @@ class DistributedOptimizer:
         else:
             self._flush_deferred_ag()
         cur = torch.cuda.current_stream(self.device)
-        for ev in self._ev_params:
-            cur.wait_event(ev)
-        self._ev_end.record(cur)
+        if wait:
+            for ev in self._ev_params:
+                cur.wait_event(ev)
+            self._ev_end.record(cur)
+        else:
+            self._ev_end.record(self.s_comm if self.backend in ("p2p", "nvls") else self.s_opt)
         self._in_step = False
         rep = StepReport(self.step_count, len(L.buckets), L.total_numel // self.dp,
                          start=self._ev_start, end=self._ev_end)
@@ -555,6 +570,7 @@ class DistributedOptimizer:
             self.s_comm.wait_event(self._ev_packed[pend[-1]])
             if self.clip is None:
                 self._p2p(pend, nat.HOD_P2P_FUSED)
+                self._span_done(pend)
             else:
                 part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * pend[0]
                 self._p2p(pend, nat.HOD_P2P_RS, partials=part)
@@ -562,8 +578,8 @@ class DistributedOptimizer:
     def _p2p_finish(self) -> None:
         nb = len(self.layout.buckets)
         s = self.s_comm
-        self._queue_p2p(None, final=True)
         if self.clip is not None:
+            self._queue_p2p(None, final=True)
             if len(self.norm_ranks) == 1:
                 nat.call("hod_sum_partials", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS,
                          _ptr(self._sumsq), nat.stream_ptr(s))
@@ -576,14 +592,33 @@ class DistributedOptimizer:
                          self._norm_d, self._norm_rank, 0, self.step_count, self.timeout_ns,
                          _ptr(self._err), ctypes.c_float(self.clip), _ptr(self._coef), _ptr(self._norm),
                          _ptr(self._sumsq), nat.stream_ptr(s))
-            for span in self._spans(range(nb)):
+            # reverse bucket order: the last bucket holds the first layers, which
+            # the next forward needs first
+            for span in reversed(self._spans(range(nb))):
                 self._p2p(span, nat.HOD_P2P_ADAMW_AG, coef_ptr=_ptr(self._coef))
-        # end-of-step barrier: every rank's param stores (and reads of our
-        # buckets) are complete before anyone uses the params or repacks
-        nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,
-                 self.step_count, self.timeout_ns, _ptr(self._err), nat.stream_ptr(s))
-        for ev in self._ev_params:
-            ev.record(s)
+                self._span_done(span)
+        else:
+            self._queue_p2p(None, final=True)
+        if not self.param_barriers:
+            # end-of-step barrier: every rank's param stores (and reads of our
+            # buckets) are complete before anyone uses the params or repacks
+            nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,
+                     self.step_count, self.timeout_ns, _ptr(self._err), nat.stream_ptr(s))
+            for ev in self._ev_params:
+                ev.record(s)
+
+    def _span_done(self, span) -> None:
+        """Per-span params-ready barrier: once every rank passed it, all peers'
+        stores into this span's param buckets (and all reads of our grad
+        buckets) are complete, so the span's params may be used / repacked."""
+        if not self.param_barriers:
+            return
+        nb = len(self.layout.buckets)
+        nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index,
+                 nb + 1 + span[0], self.step_count, self.timeout_ns, _ptr(self._err),
+                 nat.stream_ptr(self.s_comm))
+        for b in span:
+            self._ev_params[b].record(self.s_comm)
 
     def check_health(self) -> None:
         """Raise DeviceError if a cross-GPU barrier timed out (synchronises)."""

@@ -88,6 +88,35 @@ def main():
             if feed_opt:
                 opt.grad_ready(i, grads[i])
 
+    bucket_of = [opt.layout.slot(i).bucket for i in range(len(gs.tensors))]
+
+    def forward(wait: bool):
+        """Next iteration's forward, registration order; with ``wait`` each
+        bucket's params are waited for just before their first use."""
+        seen = set()
+        for i, t in enumerate(gs.tensors):
+            b = bucket_of[i]
+            if wait and b not in seen:
+                opt.wait_params(b)
+                seen.add(b)
+            if len(t.shape) == 2 and not (t.name.endswith("embed.weight") or "embed_tokens" in t.name):
+                out_f, in_f = t.shape
+                torch.matmul(acts[in_f], opt.params[i].t())          # Y = X @ W^T
+            else:
+                acts_small = opt.params[i].reshape(-1)[:1024].float().sum()  # noqa: F841  (gather stand-in)
+
+    def iteration_ref():
+        forward(False)
+        backward(False)
+
+    def iteration_ovl():
+        carve(True)
+        forward(True)
+        opt.begin_step()
+        backward(True)
+        opt.finish_step(wait=False)   # the next forward waits bucket by bucket
+        carve(False)
+
     def timed(fn):
         if world > 1:
             dist.barrier()
@@ -133,6 +162,12 @@ def main():
     t_bwd_carved = timed(backward_carved) if a.sm_budget else t_bwd
     t_opt = timed(lambda: opt.step(grads))
     t_ovl = timed(overlapped)
+    for _ in range(2):
+        iteration_ref()
+        iteration_ovl()
+    torch.cuda.synchronize()
+    t_it_ref = timed(iteration_ref)
+    t_it_ovl = timed(iteration_ovl)
     # one instrumented overlapped step: where did the optimizer kernels run?
     base = torch.cuda.Event(enable_timing=True)
     end_bwd = torch.cuda.Event(enable_timing=True)
@@ -168,6 +203,9 @@ def main():
                         "opt_kernel_ms_inside_backward": round(busy_in_bwd, 3),
                         "opt_kernel_ms_total": round(busy_total, 3)},
            "t_overlapped_ms": round(t_ovl, 3), "exposed_ms": round(exposed, 3),
+           "iteration": {"t_fwd_bwd_ms": round(t_it_ref, 3), "t_fwd_bwd_opt_ms": round(t_it_ovl, 3),
+                         "exposed_ms": round(max(0.0, t_it_ovl - t_it_ref), 3),
+                         "exposed_frac": round(max(0.0, t_it_ovl - t_it_ref) / t_it_ovl, 4)},
            "exposed_frac_of_step": round(exposed / t_ovl, 4),
            "hidden_frac_of_optimizer": round(1 - exposed / t_opt, 4) if t_opt > 0 else None,
            "backward_tflops": round(flops / (t_bwd / 1e3) / 1e12, 1)}
