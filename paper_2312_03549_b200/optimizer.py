@@ -140,7 +140,11 @@ class DistributedOptimizer:
             # NVLS from d = 4 (measured 6.61 vs 6.80 ms/step at d = 4), and at
             # d = 8 it moves 18n instead of 28n bytes per direction per GPU
             # (falls back to p2p when multicast is unavailable)
-            backend = "none" if self.dp == 1 else ("nvls" if self.dp >= 4 else "p2p")
+            # With clipping the RS and the update+AG run as separate phases around
+            # the global norm; alone, each NVLS phase is lopsided (RS: 2P out,
+            # AG: 2P in per GPU) while p2p moves 2P(d-1)/d each way, so clip -> p2p.
+            backend = ("none" if self.dp == 1 else
+                       ("nvls" if self.dp >= 4 and clip is None else "p2p"))
         if backend not in BACKENDS:
             raise InfeasibleConfigError(f"unknown backend {backend!r} (choose from {BACKENDS})")
         if (backend == "none") != (self.dp == 1):
