@@ -61,6 +61,18 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 // mapping, i.e. every state load fetched twice the sectors it used).
 constexpr int kChunk = 256;
 
+// Which 256-element chunks this warp processes: all warps of the grid stride
+// the range together.  (A blocked variant — each CTA streaming its own
+// contiguous run — measured 4-12 % slower on B200; tools/sweep_grid.sh.)
+struct ChunkRange {
+  int64_t first, last, step;
+};
+
+__device__ __forceinline__ ChunkRange chunk_range(int64_t n_chunks) {
+  const int64_t n_warps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  return ChunkRange{(static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5, n_chunks, n_warps};
+}
+
 __device__ __forceinline__ void ld_f32_quads(const float* p, int64_t e0, float (&x)[8]) {
   const float4 a = *reinterpret_cast<const float4*>(p + e0);
   const float4 b = *reinterpret_cast<const float4*>(p + e0 + 128);

@@ -152,16 +152,19 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
     float* __restrict__ m, float* __restrict__ v, uint16_t* __restrict__ out, const AdamWConsts c,
     const float* __restrict__ coef_ptr) {
   const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
-  const int64_t n_tiles = (numel + kFusedTile - 1) / kFusedTile;
+  // warp-strided 256-element chunks (same mapping as adamw_vec_kernel); the
+  // table lookup is warp-uniform and the cursor only moves forward
+  const int lane = threadIdx.x & 31;
+  const int64_t n_chunks = (numel + kChunk - 1) / kChunk;
+  ChunkRange r = chunk_range(n_chunks);
   int e = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t a = tile * kFusedTile;
-    const int64_t b = min(a + kFusedTile, numel);
-    while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;  // CTA-uniform
+  for (int64_t ch = r.first; ch < r.last; ch += r.step) {
+    const int64_t a = ch * kChunk;
+    const int64_t b = min(a + kChunk, numel);
+    while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;  // warp-uniform
     const bool inside = e < t.n && t.off[e] <= a && b <= t.off[e] + t.numel[e];
-    if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kFusedTile) {
-      // warp w owns elements [a + 256w, a + 256w + 256): lane quads at 4l and 128 + 4l
-      const int64_t e0 = a + (threadIdx.x >> 5) * kChunk + (threadIdx.x & 31) * 4;
+    if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kChunk) {
+      const int64_t e0 = a + lane * 4;
       float g[8], pf[8], mf[8], vf[8];
       if constexpr (sizeof(SrcT) == 2) ld_bf16_quads(static_cast<const uint16_t*>(t.src[e]), e0 - t.off[e], g);
       else ld_f32_quads(static_cast<const float*>(t.src[e]), e0 - t.off[e], g);
@@ -180,7 +183,7 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
       st_bf16_quads(out, e0, pf);
     } else {
       int ei = e;
-      for (int64_t i = a + threadIdx.x; i < b; i += kThreads) {
+      for (int64_t i = a + lane; i < b; i += 32) {
         while (ei < t.n && t.off[ei] + t.numel[ei] <= i) ++ei;
         float gi = 0.0f;
         if (ei < t.n && t.off[ei] <= i)
@@ -207,8 +210,8 @@ __global__ void __launch_bounds__(kThreads) adamw_vec_kernel(
     const AdamWConsts c, const float* __restrict__ coef_ptr) {
   const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
   const int lane = threadIdx.x & 31;
-  const int64_t n_warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
-  for (int64_t ch = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; ch < n_chunks; ch += n_warps) {
+  ChunkRange r = chunk_range(n_chunks);
+  for (int64_t ch = r.first; ch < r.last; ch += r.step) {
     const int64_t e0 = ch * kChunk + lane * 4;
     float gf[8], pf[8], mf[8], vf[8];
     if constexpr (sizeof(GradT) == 2) ld_bf16_quads(reinterpret_cast<const uint16_t*>(g), e0, gf);
@@ -443,7 +446,8 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   return for_each_window("hod_pack_adamw", entries, n_entries, bucket_numel, src_dtype,
                          [&](const PackTable& t, int64_t lo, int64_t span) {
-    const int grid = grid_for((span + kFusedTile - 1) / kFusedTile, 1, 3);  // measured best: 3/SM
+    // 3 CTAs/SM measured best for this kernel (2: -9 %, 4: -9 %; tools/sweep_grid.sh)
+    const int grid = grid_for((span + kChunk - 1) / kChunk * 32, kThreads, 3);
     count_launch(1);
 #define HOD_PA_LAUNCH(T, CLIP) \
     pack_adamw_kernel<T, CLIP><<<grid, kThreads, 0, s>>>(t, span, scale, master + lo, exp_avg + lo, \
