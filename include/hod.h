@@ -212,6 +212,14 @@ int hod_p2p_step(const hod_p2p_span* span, int mode, const hod_adamw_params* hp,
 int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
                     unsigned long long timeout_ns, uint32_t* err, void* stream);
 
+/* One-directional hand-off between two GPUs (pipeline activations, §8f.3):
+ * hod_p2p_signal stores `epoch` into a peer-mapped flag once all prior work of
+ * `stream` is complete (system fence); hod_p2p_wait makes `stream` wait (1
+ * thread, bounded spin, HOD_ETIMEOUT into *err) until the local flag >= epoch. */
+int hod_p2p_signal(uint32_t* peer_flag, uint32_t epoch, void* stream);
+int hod_p2p_wait(const uint32_t* flag, uint32_t epoch, unsigned long long timeout_ns, uint32_t* err,
+                 void* stream);
+
 /* global norm over d ranks through peer memory: fixed-order sum of this rank's
  * partials, publish to xchg[q][rank] (fp64) of every rank, barrier, rank-order
  * sum => identical deterministic coef/norm on all ranks. */

@@ -326,6 +326,25 @@ __global__ void norm_exchange_kernel(const float* partials, int64_t n_partials, 
   }
 }
 
+// One-directional hand-off for pipeline point-to-point transfers (§8f.3):
+// the producer signals after its payload copy is complete (stream order +
+// system fence), the consumer's stream waits until the flag reaches `epoch`.
+__global__ void signal_kernel(uint32_t* peer_flag, uint32_t epoch) {
+  __threadfence_system();
+  st_release_sys(peer_flag, epoch);
+}
+
+__global__ void wait_kernel(const uint32_t* flag, uint32_t epoch, unsigned long long timeout_ns, uint32_t* err) {
+  const unsigned long long t0 = globaltimer();
+  while (static_cast<int32_t>(ld_acquire_sys(flag) - epoch) < 0) {
+    if (globaltimer() - t0 > timeout_ns) {
+      if (err) atomicExch(err, static_cast<uint32_t>(HOD_ETIMEOUT));
+      return;
+    }
+    __nanosleep(200);
+  }
+}
+
 static int unroll_setting() {
   static int u = [] {
     const char* e = getenv("HOD_P2P_UNROLL");
@@ -447,6 +466,22 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
     if (nv) dispatch_d<true, 2>(a, b, c, sp->rank, grid, s); else dispatch_d<false, 2>(a, b, c, sp->rank, grid, s);
   }
   return cuda_status(cudaGetLastError(), "hod_p2p_step launch");
+}
+
+int hod_p2p_signal(uint32_t* peer_flag, uint32_t epoch, void* stream) {
+  if (!peer_flag) { set_error("hod_p2p_signal: null flag"); return HOD_EINVAL; }
+  count_launch(1);
+  signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(peer_flag, epoch);
+  return cuda_status(cudaGetLastError(), "hod_p2p_signal launch");
+}
+
+int hod_p2p_wait(const uint32_t* flag, uint32_t epoch, unsigned long long timeout_ns, uint32_t* err,
+                 void* stream) {
+  if (!flag) { set_error("hod_p2p_wait: null flag"); return HOD_EINVAL; }
+  count_launch(1);
+  wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, epoch,
+                                                             timeout_ns ? timeout_ns : 20000000000ull, err);
+  return cuda_status(cudaGetLastError(), "hod_p2p_wait launch");
 }
 
 int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,

@@ -564,6 +564,9 @@ class DistributedOptimizer:
     def _queue_p2p(self, bi: int, final: bool = False) -> None:
         """Bucket bi is packed: extend the pending span, launch it when full."""
         if bi is not None:
+            if self._pending_span and bi != self._pending_span[-1] + 1:
+                # spans must be consecutive buckets (their state is contiguous)
+                self._queue_p2p(None, final=True)
             self._pending_span.append(bi)
         pend = self._pending_span
         full = (sum(self.layout.buckets[x].numel for x in pend) >= self.span_numel

@@ -196,3 +196,26 @@ def test_pp_dp_scenario_parity(oracle, tmp_path, backend, clip):
                 oracle.adamw(master, mm, vv, d["reduced"], step, coef=float(d["coef"]) if clip else None)
                 np.testing.assert_array_equal(master.view(np.uint32), d["master"].view(np.uint32))
                 np.testing.assert_array_equal(vv.view(np.uint32), d["v"].view(np.uint32))
+
+
+def test_pipeline_1f1b_handoffs_over_peer_memory(tmp_path):
+    """§8f.3: activations / activation gradients cross the emulated cluster
+    boundary in the 1F1B order of simulator._one_f_one_b; each hand-off lands
+    intact (compute stand-in: +1 per stage per direction)."""
+    if _ngpus() < 4:
+        pytest.skip("needs 4 GPUs")
+    scen = tmp_path / "mini_pp.json"
+    scen.write_text(json.dumps(MINI_PP_SCENARIO))
+    args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
+            "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+            str(ROOT / "tests" / "mp_worker_pipeline.py"), "--scenario", str(scen), "--out", str(tmp_path),
+            "--micro", "4", "--iters", "2"]
+    r = subprocess.run(args, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    for q in range(4):
+        doc = json.loads((tmp_path / f"pipe_r{q}.json").read_text())
+        tr = doc["trace"]
+        assert len(tr) == 2 * 4                        # 4 micro-batches x 2 iterations, one direction
+        for op, k, mean, std in tr:
+            # stage 1 sends x + 1 = 2; stage 2 returns (2 + 1) + 1 = 4
+            assert (op, mean, std) == (("fwd", 2.0, 0.0) if doc["stage"] == 2 else ("bwd", 4.0, 0.0))
