@@ -44,6 +44,7 @@ def main():
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--backend", default="nccl")
     ap.add_argument("--out", required=True)
+    ap.add_argument("--final-only", type=int, default=0, help="dump only the state after the last step")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
@@ -59,6 +60,9 @@ def main():
     L = opt.layout
     out = Path(a.out)
     for step in range(1, a.steps + 1):
+        if a.final_only and step < a.steps:
+            opt.step(make_grads(gs, step, rank, dev, dtype=gdt))
+            continue
         # state BEFORE the step (so the oracle can replay it exactly)
         pre = dict(master=opt.master.cpu().numpy().copy(), m=opt.exp_avg.cpu().numpy().copy(),
                    v=opt.exp_avg_sq.cpu().numpy().copy())

@@ -219,3 +219,51 @@ def test_pipeline_1f1b_handoffs_over_peer_memory(tmp_path):
         for op, k, mean, std in tr:
             # stage 1 sends x + 1 = 2; stage 2 returns (2 + 1) + 1 = 4
             assert (op, mean, std) == (("fwd", 2.0, 0.0) if doc["stage"] == 2 else ("bwd", 4.0, 0.0))
+
+
+@pytest.mark.parametrize("backend", ["p2p", "nccl"])
+def test_100_steps_multi_rank_against_oracle(oracle, tmp_path, backend):
+    """North-star tolerance at d = 2: after 100 steps the fp32 master and both
+    moments match the oracle's independent 100-step replay (rank-order fp32
+    reduce-scatter) — bit-exactly for the deterministic p2p backend, within
+    1e-5 (norm-relative) for NCCL."""
+    n = 2
+    if _ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    steps, bucket = 100, 1_000_000
+    run_workers(tmp_path, n, config="odd", grad_dtype="bf16", bucket=bucket, clip=0.0, steps=steps,
+                backend=backend, final_only=1)
+    from paper_2312_03549_b200.buckets import build_bucket_layout
+
+    gs = config_gradset("odd")
+    L = build_bucket_layout(gs.numels, bucket, dp=n)
+    from paper_2312_03549_b200.optimizer import fill_master_shards
+    from paper_2312_03549_b200.synthetic import init_params
+
+    p0 = init_params(gs, "cuda:0")
+    state = []
+    for r in range(n):
+        master = torch.zeros(L.total_numel // n)
+        fill_master_shards(L, [p.cpu() for p in p0], r, master)
+        state.append([master.numpy().copy(), np.zeros(L.total_numel // n, np.float32),
+                      np.zeros(L.total_numel // n, np.float32)])
+    offs = L.shard_offsets()
+    for step in range(1, steps + 1):
+        grads = [[u16(g).reshape(-1) for g in make_grads(gs, step, q, "cuda:0")] for q in range(n)]
+        for bi, b in enumerate(L.buckets):
+            packs = [oracle.pack([grads[q][s.index] for s in b.slots], [s.offset for s in b.slots], b.numel,
+                                 1.0 / n) for q in range(n)]
+            sh = b.numel // n
+            for r in range(n):
+                red = oracle.reduce_scatter(packs, r, n)
+                m_, mm, vv = (x[offs[bi]:offs[bi] + sh] for x in state[r])
+                oracle.adamw(m_, mm, vv, red, step)
+    for r in range(n):
+        d = np.load(tmp_path / f"r{r}_s{steps}.npz")
+        for name, want in zip(("master", "m", "v"), state[r]):
+            got = d[name]
+            if backend == "p2p":
+                np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+            else:
+                err = np.abs(got.astype(np.float64) - want).max()
+                assert err <= 1e-5 * np.abs(want).max(), (name, err)
