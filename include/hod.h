@@ -106,6 +106,13 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
                    float* exp_avg_sq, uint16_t* param, const hod_adamw_params* hp,
                    const float* clip_coef, void* stream);
 
+/* Sum of squares of the values the packed bucket would hold (bf16_rne(src*scale),
+ * 0 in gaps), read straight from the tensors: HOD_SUMSQ_PARTIALS fixed-grid
+ * partials, at most HOD_PACK_MAX_ENTRIES entries.  d == 1 with clipping:
+ * norm pass (2 B/element) then hod_pack_adamw with the clip coefficient. */
+int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel,
+                   float scale, int src_dtype, float* partials, void* stream);
+
 /* ---- K3: deterministic sum of squares of a bf16 shard -----
  * Writes HOD_SUMSQ_PARTIALS fp32 partial sums to partials[0..HOD_SUMSQ_PARTIALS)
  * (fixed grid, fixed order => bit-reproducible for a given n). */

@@ -23,7 +23,7 @@ HOD_DTYPE_F32 = 1
 # every symbol include/hod.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
-    "hod_pack_bf16", "hod_pack_adamw", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
+    "hod_pack_bf16", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
     "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
@@ -92,6 +92,7 @@ def load(build_if_missing: bool = True):
         "hod_pack_adamw": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, P, P, P,
                             ctypes.POINTER(AdamWParams), P, P], I),
         "hod_sum_partials": ([P, I64, P, P], I),
+        "hod_pack_sumsq": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, P], I),
         "hod_clip_coef": ([P, F, P, P, P], I),
         "hod_adamw_bf16": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
         "hod_adamw_f32": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),

@@ -34,6 +34,14 @@ __device__ __forceinline__ uint16_t f32_to_bf16(float f) {
   return static_cast<uint16_t>(u >> 16);
 }
 
+// Hardware RNE of two fp32 to bf16x2 (lo in bits 0-15).  A NaN becomes the
+// canonical NaN, so use it only where NaN payload bits do not matter (norms).
+__device__ __forceinline__ uint32_t cvt_bf16x2_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 // Unpack 8 bf16 from a uint4 into floats.
 __device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
   const uint32_t w[4] = {q.x, q.y, q.z, q.w};

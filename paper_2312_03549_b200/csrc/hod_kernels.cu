@@ -291,20 +291,28 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
 // K3: sum of squares with a FIXED grid of HOD_SUMSQ_PARTIALS CTAs so the
 // per-CTA partials (and their fixed-order final sum) are reproducible.
 // ---------------------------------------------------------------------------
+// The partials grid is only HOD_SUMSQ_PARTIALS (2 per SM) CTAs, so these
+// read-only streams use 1024-thread CTAs to fill the SM (2048 threads).
+constexpr int kSumsqThreads = 1024;
+constexpr int kSumsqUnroll = 2;
+constexpr int kSumsqTile = kSumsqThreads * kPackVec * kSumsqUnroll;   // 16384 elements
+
+template <int NT>
 __device__ __forceinline__ float block_sum(float x) {
-  __shared__ float warp_part[kThreads / 32];
+  __shared__ float warp_part[NT / 32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   if ((threadIdx.x & 31) == 0) warp_part[threadIdx.x >> 5] = x;
   __syncthreads();
   float s = 0.0f;
   if (threadIdx.x == 0)
-    for (int w = 0; w < kThreads / 32; ++w) s += warp_part[w];
+    for (int w = 0; w < NT / 32; ++w) s += warp_part[w];
   return s;  // valid on thread 0
 }
 
-__global__ void __launch_bounds__(kThreads) sumsq_kernel(const uint16_t* __restrict__ x, int64_t n,
-                                                          bool vec, float* __restrict__ partials) {
+__global__ void __launch_bounds__(kSumsqThreads) sumsq_kernel(const uint16_t* __restrict__ x, int64_t n,
+                                                               bool vec, float* __restrict__ partials) {
+  constexpr int kThreads = kSumsqThreads;
   float acc = 0.0f;
   const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
   int64_t tail_begin = 0;
@@ -322,8 +330,69 @@ __global__ void __launch_bounds__(kThreads) sumsq_kernel(const uint16_t* __restr
     const float f = bf16_to_f32(x[i]);
     acc = __fadd_rn(acc, __fmul_rn(f, f));
   }
-  const float s = block_sum(acc);
+  const float s = block_sum<kSumsqThreads>(acc);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
+  if (blockIdx.x == 0)
+    for (int i = gridDim.x + threadIdx.x; i < HOD_SUMSQ_PARTIALS; i += blockDim.x) partials[i] = 0.0f;
+}
+
+// Sum of squares of the PACKED gradient, read straight from the tensors (the
+// values bf16_rne(src*scale) the bucket would hold; 0 in gaps) — d == 1 with
+// clipping needs the norm before the fused pack+AdamW, and this pass costs
+// 2 B/element instead of the 4 + 2 of pack-then-sumsq.  Fixed grid, fixed
+// per-thread order => reproducible partials.
+template <typename SrcT>
+__global__ void __launch_bounds__(kSumsqThreads) pack_sumsq_kernel(const __grid_constant__ PackTable t,
+                                                                    int64_t numel, float scale,
+                                                                    float* __restrict__ partials) {
+  constexpr int kThreads = kSumsqThreads;
+  constexpr int kPackTile = kSumsqTile;
+  // 8 independent accumulators (one per vector lane), folded in a fixed order
+  // at the end: breaks the serial FADD chain, stays reproducible
+  float acc8[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+  // a bf16 source times 1.0 is already its own bf16 rounding
+  const bool exact = sizeof(SrcT) == 2 && scale == 1.0f;
+  const int64_t n_tiles = (numel + kPackTile - 1) / kPackTile;
+  int e = 0;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t a = tile * kPackTile;
+    const int64_t b = min(a + kPackTile, numel);
+    while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;
+    const bool inside = e < t.n && t.off[e] <= a && b <= t.off[e] + t.numel[e];
+    if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kPackTile) {
+      const int64_t s0 = a - t.off[e];
+#pragma unroll
+      for (int u = 0; u < kSumsqUnroll; ++u) {
+        float f[8];
+        load8<SrcT>(t.src[e], s0 + (static_cast<int64_t>(u) * kThreads + threadIdx.x) * kPackVec, f);
+        if (!exact) {
+          // g = bf16_rne(src * scale), two at a time on the converter
+#pragma unroll
+          for (int k = 0; k < 8; k += 2) {
+            const uint32_t r = cvt_bf16x2_rn(__fmul_rn(f[k], scale), __fmul_rn(f[k + 1], scale));
+            f[k] = __uint_as_float(r << 16);
+            f[k + 1] = __uint_as_float(r & 0xffff0000u);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) acc8[k] = __fadd_rn(acc8[k], __fmul_rn(f[k], f[k]));
+      }
+    } else {
+      int ei = e;
+      for (int64_t i = a + threadIdx.x; i < b; i += kThreads) {
+        while (ei < t.n && t.off[ei] + t.numel[ei] <= i) ++ei;
+        if (ei < t.n && t.off[ei] <= i) {
+          const float g = bf16_to_f32(f32_to_bf16(__fmul_rn(load_src<SrcT>(t.src[ei], i - t.off[ei]), scale)));
+          acc8[0] = __fadd_rn(acc8[0], __fmul_rn(g, g));
+        }
+      }
+    }
+  }
+  float acc = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) acc = __fadd_rn(acc, acc8[k]);
+  const float sblk = block_sum<kSumsqThreads>(acc);
+  if (threadIdx.x == 0) partials[blockIdx.x] = sblk;
   if (blockIdx.x == 0)
     for (int i = gridDim.x + threadIdx.x; i < HOD_SUMSQ_PARTIALS; i += blockDim.x) partials[i] = 0.0f;
 }
@@ -462,10 +531,30 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
   });
 }
 
+int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel, float scale,
+                   int src_dtype, float* partials, void* stream) {
+  if (!partials) { set_error("hod_pack_sumsq: null partials"); return HOD_EINVAL; }
+  if (n_entries > HOD_PACK_MAX_ENTRIES) {
+    set_error("hod_pack_sumsq: at most %d entries per call", HOD_PACK_MAX_ENTRIES); return HOD_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (bucket_numel == 0) return hod_sumsq_bf16(nullptr, 0, partials, stream);
+  return for_each_window("hod_pack_sumsq", entries, n_entries, bucket_numel, src_dtype,
+                         [&](const PackTable& t, int64_t lo, int64_t span) {
+    count_launch(1);
+    if (src_dtype == HOD_DTYPE_BF16)
+      pack_sumsq_kernel<uint16_t><<<partials_grid(), kSumsqThreads, 0, s>>>(t, span, scale, partials);
+    else
+      pack_sumsq_kernel<float><<<partials_grid(), kSumsqThreads, 0, s>>>(t, span, scale, partials);
+    (void)lo;
+    return cuda_status(cudaGetLastError(), "hod_pack_sumsq launch");
+  });
+}
+
 int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) {
   if (!partials || n < 0 || (n > 0 && !x)) { set_error("hod_sumsq_bf16: bad arguments"); return HOD_EINVAL; }
   count_launch(1);
-  sumsq_kernel<<<partials_grid(), kThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
+  sumsq_kernel<<<partials_grid(), kSumsqThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
   return cuda_status(cudaGetLastError(), "hod_sumsq_bf16 launch");
 }
 

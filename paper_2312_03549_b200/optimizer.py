@@ -285,6 +285,7 @@ class DistributedOptimizer:
         self._launched = [False] * nb
         self._deferred_ag = []
         self._pending_span = []
+        self._deferred_pa = []
         self._ev_start.record(torch.cuda.current_stream(self.device))
         if self.clip is not None and self.backend in ("p2p", "nvls"):
             # span starts (hence the partial slots written) may differ between steps
@@ -316,6 +317,8 @@ class DistributedOptimizer:
                 raise InfeasibleConfigError(f"bucket {b} is missing gradients for params {missing[:8]}")
         if self.backend in ("p2p", "nvls"):
             self._p2p_finish()
+        elif self._deferred_pa:
+            self._norm_then_pack_adamw()
         elif self.clip is not None:
             self._clip_and_update()
         else:
@@ -428,18 +431,21 @@ class DistributedOptimizer:
             entries[k].dst_offset = s.offset
         bucket_ptr = _ptr(self.grad_buffer) + 2 * b.start
         src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
-        if self.backend == "none" and self.clip is None and not self.keep_reduced:
-            # d == 1: nothing to exchange, so K1 and K2 fuse (no bucket round trip)
-            off = self._shard_off[bi]
-            hp = self._hp()
-            t0 = self._timed_event(self.s_pack)
-            nat.call("hod_pack_adamw", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale),
-                     dtype, _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
-                     _ptr(self.exp_avg_sq) + 4 * off, _ptr(self.param_buffer) + 2 * b.start,
-                     ctypes.byref(hp), None, nat.stream_ptr(self.s_pack))
-            self._timed_close("pack_adamw", t0, self.s_pack, (src_bytes + 26) * b.numel)
-            self._ev_params[bi].record(self.s_pack)
+        if self.backend == "none" and not self.keep_reduced and (
+                self.clip is None or len(b.slots) <= nat.HOD_PACK_MAX_ENTRIES):
+            # d == 1: nothing to exchange, so K1 and K2 fuse (no bucket round
+            # trip).  With clipping the norm needs every bucket first: a
+            # 2 B/element norm pass now, the fused update after the norm.
             self._launched[bi] = True
+            if self.clip is None:
+                self._pack_adamw(bi, entries, dtype, None)
+                return
+            part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * bi
+            t0 = self._timed_event(self.s_pack)
+            nat.call("hod_pack_sumsq", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale),
+                     dtype, part, nat.stream_ptr(self.s_pack))
+            self._timed_close("pack_sumsq", t0, self.s_pack, src_bytes * b.numel)
+            self._deferred_pa.append((bi, entries, dtype))
             return
         t0 = self._timed_event(self.s_pack)
         nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
@@ -468,6 +474,19 @@ class DistributedOptimizer:
             self._update_bucket(bi, reduced, clip_coef_ptr=None)
             # all-gather of the previous bucket goes behind this RS (pipelining)
             self._flush_deferred_ag(keep_last=True)
+
+    def _pack_adamw(self, bi: int, entries, dtype, coef_ptr) -> None:
+        b = self.layout.buckets[bi]
+        off = self._shard_off[bi]
+        hp = self._hp()
+        src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
+        t0 = self._timed_event(self.s_pack)
+        nat.call("hod_pack_adamw", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale),
+                 dtype, _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
+                 _ptr(self.exp_avg_sq) + 4 * off, _ptr(self.param_buffer) + 2 * b.start,
+                 ctypes.byref(hp), coef_ptr, nat.stream_ptr(self.s_pack))
+        self._timed_close("pack_adamw", t0, self.s_pack, (src_bytes + 26) * b.numel)
+        self._ev_params[bi].record(self.s_pack)
 
     def _update_bucket(self, bi: int, ready: torch.cuda.Event, clip_coef_ptr) -> None:
         b = self.layout.buckets[bi]
@@ -635,6 +654,19 @@ class DistributedOptimizer:
                 from .errors import DeviceError
 
                 raise DeviceError(f"fused collective reported error {code} (barrier timeout)")
+
+    def _norm_then_pack_adamw(self) -> None:
+        """d == 1 with clipping: every bucket's norm partials exist; finish the
+        norm on the pack stream and run the fused pack+AdamW per bucket."""
+        nb = len(self.layout.buckets)
+        s = self.s_pack
+        nat.call("hod_sum_partials", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS,
+                 _ptr(self._sumsq), nat.stream_ptr(s))
+        nat.call("hod_clip_coef", _ptr(self._sumsq), ctypes.c_float(self.clip), _ptr(self._coef),
+                 _ptr(self._norm), nat.stream_ptr(s))
+        for bi, entries, dtype in self._deferred_pa:
+            self._pack_adamw(bi, entries, dtype, _ptr(self._coef))
+        self._deferred_pa = []
 
     def _clip_and_update(self) -> None:
         nb = len(self.layout.buckets)

@@ -171,6 +171,37 @@ def test_sumsq_deterministic_and_close(oracle, native):
     assert coef.item() == oracle.clip_coef(np.float32(a), 1.0)
 
 
+@pytest.mark.parametrize("src_dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("scale", [1.0, 1.0 / 3.0])
+def test_pack_sumsq_matches_packed_norm(oracle, native, src_dtype, scale):
+    """hod_pack_sumsq (d = 1 clip norm read straight from the tensors) equals the
+    sum of squares of the oracle's packed bucket, gaps and padding included."""
+    gs = odd_tensors()
+    layout = build_bucket_layout(gs.numels, 150_000, dp=1)
+    gen = torch.Generator(device=DEV).manual_seed(9)
+    grads = [torch.randn(t.shape, generator=gen, device=DEV).mul_(1e-2).to(src_dtype)
+             for t in gs.tensors]
+    parts = torch.empty(nat.HOD_SUMSQ_PARTIALS, device=DEV)
+    out = torch.empty(2, device=DEV)
+    for b in layout.buckets:
+        gl = [grads[s.index].reshape(-1) for s in b.slots]
+        offs = [s.offset for s in b.slots]
+        entries = (nat.PackEntry * len(gl))()
+        for k, (g, off) in enumerate(zip(gl, offs)):
+            entries[k].src, entries[k].numel, entries[k].dst_offset = g.data_ptr(), g.numel(), off
+        dtype = nat.HOD_DTYPE_F32 if src_dtype == torch.float32 else nat.HOD_DTYPE_BF16
+        for k in range(2):
+            nat.call("hod_pack_sumsq", entries, len(gl), b.numel, ctypes.c_float(scale), dtype,
+                     parts.data_ptr(), 0)
+            nat.call("hod_sum_partials", parts.data_ptr(), nat.HOD_SUMSQ_PARTIALS, out[k:].data_ptr(), 0)
+        torch.cuda.synchronize()
+        a, a2 = out.cpu().numpy()
+        assert a == a2  # bit-reproducible
+        cpu = [g.cpu().numpy() if src_dtype == torch.float32 else u16(g) for g in gl]
+        want = oracle.sumsq_bf16(oracle.pack(cpu, offs, b.numel, scale))
+        assert abs(a - want) <= 1e-5 * want
+
+
 def test_bad_arguments_raise_device_error(native):
     from paper_2312_03549_b200.errors import DeviceError
 

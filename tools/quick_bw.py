@@ -59,3 +59,17 @@ for lim in (148, 74, 48, 32, 16):
                                 out.data_ptr(), n, ctypes.byref(hp), None, 0))
     nat.call("hod_set_grid_limit", 0)
     print(f"adamw_vec ctas={lim * 4} (~{lim} SMs): {t:.3f} ms  {28 * n / t / 1e6:.0f} GB/s")
+
+# bucket-sized launches (LLaMA-7B: ~33.5M-element buckets of 1-3 tensors)
+nb = 33_554_432
+srcs = [torch.randn(nb // 2, device=dev).to(torch.bfloat16) for _ in range(2)]
+eb = (nat.PackEntry * 2)()
+for k, t_ in enumerate(srcs):
+    eb[k].src, eb[k].numel, eb[k].dst_offset = t_.data_ptr(), t_.numel(), k * (nb // 2)
+t = timeit(lambda: nat.call("hod_pack_sumsq", eb, 2, nb, ctypes.c_float(1.0), 0, parts.data_ptr(), 0), 50)
+print(f"pack_sumsq bucket n={nb}: {t * 1e3:.1f} us  {2 * nb / t / 1e6:.0f} GB/s")
+t = timeit(lambda: nat.call("hod_sumsq_bf16", g.data_ptr(), nb, parts.data_ptr(), 0), 50)
+print(f"sumsq bucket n={nb}: {t * 1e3:.1f} us  {2 * nb / t / 1e6:.0f} GB/s")
+t = timeit(lambda: nat.call("hod_pack_adamw", eb, 2, nb, ctypes.c_float(1.0), 0, p.data_ptr(), m.data_ptr(),
+                            v.data_ptr(), out.data_ptr(), ctypes.byref(hp), None, 0), 50)
+print(f"pack_adamw bucket n={nb}: {t * 1e3:.1f} us  {28 * nb / t / 1e6:.0f} GB/s")
