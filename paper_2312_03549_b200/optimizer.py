@@ -31,6 +31,7 @@ overlapped operation.  The ``backend`` selects how C1/C2 move bytes:
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -122,7 +123,7 @@ class DistributedOptimizer:
                  device=None, param_align: int = 64, process_group=None, norm_group=None,
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
                  sm_budget: int | None = None, span_numel: int = 128 * 2**20,
-                 param_barriers: bool = True):
+                 param_barriers: bool = True, pre_barrier: bool | None = None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -163,6 +164,20 @@ class DistributedOptimizer:
         # wait_params for a forward-overlapped all-gather) instead of a single
         # end-of-step barrier
         self.param_barriers = bool(param_barriers)
+        # arrival barrier as a 1-CTA kernel ahead of each RS/fused span launch:
+        # the wide kernel then never occupies SMs while a late peer catches up.
+        # Measured trade-off (profiles/r01_overlap_prebarrier.jsonl): exposed
+        # share of a training iteration drops at d = 2 14.1 -> 12.8 % (1.3B),
+        # 11.3 -> 9.7 % (LLaMA-7B clip), at d = 4 10.5 -> 9.4 % and 7.4 ->
+        # 6.2 %, but the standalone step pays ~20 us per span (LLaMA-7B
+        # d = 4: 34.7 -> 35.4 ms).  Default (None): on once the optimizer is
+        # driven by autograd hooks (register_hooks: backward kernels share the
+        # SMs), off for resident-gradient steps; env HOD_PRE_BARRIER=0/1 forces.
+        env = os.environ.get("HOD_PRE_BARRIER")
+        if env is not None:
+            pre_barrier = env == "1"
+        self._pre_barrier_auto = pre_barrier is None
+        self.pre_barrier = bool(pre_barrier)
         self._pending_span: list[int] = []
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
@@ -372,6 +387,8 @@ class DistributedOptimizer:
         """Attach post-accumulate-grad hooks: parameter i's gradient feeds
         ``grad_ready(i)``.  ``module_params[i]`` must be the model parameter
         for registration index i."""
+        if self._pre_barrier_auto:
+            self.pre_barrier = True
         handles = []
         for i, p in enumerate(module_params):
             def hook(param, i=i):
@@ -475,18 +492,24 @@ class DistributedOptimizer:
             # all-gather of the previous bucket goes behind this RS (pipelining)
             self._flush_deferred_ag(keep_last=True)
 
-    def _pack_adamw(self, bi: int, entries, dtype, coef_ptr) -> None:
+    def _pack_adamw(self, bi: int, entries, dtype, coef_ptr, last: int | None = None) -> None:
+        """Fused pack+AdamW (d == 1) over buckets bi..last (default bi): at d = 1
+        consecutive buckets are one contiguous range of the flat buffers, so a
+        run of them is a single launch (``entries`` offsets relative to bucket bi)."""
+        last = bi if last is None else last
         b = self.layout.buckets[bi]
+        numel = self.layout.buckets[last].start + self.layout.buckets[last].numel - b.start
         off = self._shard_off[bi]
         hp = self._hp()
         src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
         t0 = self._timed_event(self.s_pack)
-        nat.call("hod_pack_adamw", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale),
+        nat.call("hod_pack_adamw", entries, len(entries), numel, ctypes.c_float(self.grad_scale),
                  dtype, _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
                  _ptr(self.exp_avg_sq) + 4 * off, _ptr(self.param_buffer) + 2 * b.start,
                  ctypes.byref(hp), coef_ptr, nat.stream_ptr(self.s_pack))
-        self._timed_close("pack_adamw", t0, self.s_pack, (src_bytes + 26) * b.numel)
-        self._ev_params[bi].record(self.s_pack)
+        self._timed_close("pack_adamw", t0, self.s_pack, (src_bytes + 26) * numel)
+        for k in range(bi, last + 1):
+            self._ev_params[k].record(self.s_pack)
 
     def _update_bucket(self, bi: int, ready: torch.cuda.Event, clip_coef_ptr) -> None:
         b = self.layout.buckets[bi]
@@ -562,6 +585,9 @@ class DistributedOptimizer:
         # algorithmic bytes per launch: local HBM (state 24 B + own param 2 B +
         # own grad 2 B per owned element) — NVLink bytes are reported separately
         nbytes = {"fused": 28 * n_total, "rs": 2 * d * n_total + 2 * n_total, "adamw_ag": 28 * n_total}[name]
+        if self.pre_barrier and mode != nat.HOD_P2P_ADAMW_AG:
+            nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), d, self.shard_index, sp.slot,
+                     sp.epoch, self.timeout_ns, _ptr(self._err), nat.stream_ptr(self.s_comm))
         t0 = self._timed_event(self.s_comm)
         nat.call("hod_p2p_step", ctypes.byref(sp), mode, ctypes.byref(hp), nat.stream_ptr(self.s_comm))
         self._timed_close(name, t0, self.s_comm, nbytes)
@@ -664,9 +690,34 @@ class DistributedOptimizer:
                  _ptr(self._sumsq), nat.stream_ptr(s))
         nat.call("hod_clip_coef", _ptr(self._sumsq), ctypes.c_float(self.clip), _ptr(self._coef),
                  _ptr(self._norm), nat.stream_ptr(s))
-        for bi, entries, dtype in self._deferred_pa:
-            self._pack_adamw(bi, entries, dtype, _ptr(self._coef))
+        # merge runs of consecutive buckets (same source dtype, <= one pack
+        # window of entries) into single launches — fewer launch tails; runs go
+        # in DESCENDING bucket order so the first layers' parameters (last
+        # bucket) are ready first for the next forward
+        L = self.layout
+        pend = sorted(self._deferred_pa, key=lambda t: t[0], reverse=True)
         self._deferred_pa = []
+        coef = _ptr(self._coef)
+        i = 0
+        while i < len(pend):
+            hi, _, dtype = pend[i]
+            lo, j, n_ent = hi, i + 1, len(pend[i][1])
+            while (j < len(pend) and pend[j][0] == lo - 1 and pend[j][2] == dtype
+                   and n_ent + len(pend[j][1]) <= nat.HOD_PACK_MAX_ENTRIES):
+                lo, n_ent, j = pend[j][0], n_ent + len(pend[j][1]), j + 1
+            if lo == hi:
+                self._pack_adamw(hi, pend[i][1], dtype, coef)
+            else:
+                base = L.buckets[lo].start
+                merged = (nat.PackEntry * n_ent)()
+                k = 0
+                for bi, entries, _ in reversed(pend[i:j]):          # ascending bucket order
+                    shift = L.buckets[bi].start - base
+                    for e in entries:
+                        merged[k].src, merged[k].numel, merged[k].dst_offset = e.src, e.numel, e.dst_offset + shift
+                        k += 1
+                self._pack_adamw(lo, merged, dtype, coef, last=hi)
+            i = j
 
     def _clip_and_update(self) -> None:
         nb = len(self.layout.buckets)

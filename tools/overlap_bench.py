@@ -46,6 +46,8 @@ def main():
     ap.add_argument("--sm-budget", type=int, default=0,
                     help="CTAs per optimizer launch during backward; the backward GEMMs get the "
                          "same number of SMs carved out (torch._C._set_sm_carveout_experimental)")
+    ap.add_argument("--pre-barrier", type=int, default=None,
+                    help="1: arrival barrier as a 1-CTA kernel before each span (optimizer pre_barrier)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -58,7 +60,8 @@ def main():
     p0 = init_params(gs, dev)
     opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None,
                                dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
-                               sm_budget=a.sm_budget or None)
+                               sm_budget=a.sm_budget or None,
+                               pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier))
     del p0
     T = a.tokens
     # 2-D weights get GEMMs; 1-D (norm) weights get a tiny elementwise grad
@@ -194,6 +197,7 @@ def main():
     flops = sum(4 * T * t.shape[0] * t.shape[1] for t in gs.tensors if len(t.shape) == 2
                 and "embed" not in t.name)
     doc = {"config": a.config, "world": world, "backend": opt.backend, "tokens_per_gpu": T,
+           "pre_barrier": opt.pre_barrier,
            "sm_budget": a.sm_budget,
            "clip": a.clip or None, "buckets": len(opt.layout.buckets), "bucket_size": a.bucket_size,
            "t_backward_ms": round(t_bwd, 3), "t_backward_carved_ms": round(t_bwd_carved, 3),
@@ -207,6 +211,10 @@ def main():
                          "exposed_ms": round(max(0.0, t_it_ovl - t_it_ref), 3),
                          "exposed_frac": round(max(0.0, t_it_ovl - t_it_ref) / t_it_ovl, 4)},
            "exposed_frac_of_step": round(exposed / t_ovl, 4),
+           # SURVEY §8d definition: optimizer/collective kernels busy while no
+           # backward kernel runs (the tail after the last backward GEMM)
+           "exposed_comm_frac_survey": round(max(0.0, max((e for _, _, e in spans), default=0.0) - bwd_end_ms)
+                                             / max((e for _, _, e in spans), default=1.0), 4),
            "hidden_frac_of_optimizer": round(1 - exposed / t_opt, 4) if t_opt > 0 else None,
            "backward_tflops": round(flops / (t_bwd / 1e3) / 1e12, 1)}
     if rank == 0:

@@ -73,3 +73,16 @@ print(f"sumsq bucket n={nb}: {t * 1e3:.1f} us  {2 * nb / t / 1e6:.0f} GB/s")
 t = timeit(lambda: nat.call("hod_pack_adamw", eb, 2, nb, ctypes.c_float(1.0), 0, p.data_ptr(), m.data_ptr(),
                             v.data_ptr(), out.data_ptr(), ctypes.byref(hp), None, 0), 50)
 print(f"pack_adamw bucket n={nb}: {t * 1e3:.1f} us  {28 * nb / t / 1e6:.0f} GB/s")
+e1 = (nat.PackEntry * 1)()
+e1[0].src, e1[0].numel, e1[0].dst_offset = g.data_ptr(), n, 0
+t = timeit(lambda: nat.call("hod_pack_adamw", e1, 1, n, ctypes.c_float(1.0), 0, p.data_ptr(), m.data_ptr(),
+                            v.data_ptr(), out.data_ptr(), ctypes.byref(hp), None, 0))
+print(f"pack_adamw 1 entry n={n}: {t:.3f} ms  {28 * n / t / 1e6:.0f} GB/s")
+for nn in (nb, 4 * nb):
+    t = timeit(lambda: nat.call("hod_adamw_bf16", p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
+                                out.data_ptr(), nn, ctypes.byref(hp), None, 0), 50)
+    print(f"adamw n={nn}: {t * 1e3:.1f} us  {28 * nn / t / 1e6:.0f} GB/s")
+    e1[0].numel = nn
+    t = timeit(lambda: nat.call("hod_pack_adamw", e1, 1, nn, ctypes.c_float(1.0), 0, p.data_ptr(), m.data_ptr(),
+                                v.data_ptr(), out.data_ptr(), ctypes.byref(hp), None, 0), 50)
+    print(f"pack_adamw 1 entry n={nn}: {t * 1e3:.1f} us  {28 * nn / t / 1e6:.0f} GB/s")
