@@ -40,6 +40,9 @@ CONFIGS = {
     "llama7b": dict(grad_dtype="bf16", clip=1.0, desc="LLaMA-7B real tensor list, bf16 grads, grad-norm clip 1.0"),
 }
 FALLBACK_HBM_GBS = 6650.0
+NVLINK_MEASURED = 770.0   # GB/s per direction per GPU, peer copy (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0    # NVLink 5, 18 links
+
 KERNEL_NAMES = {
     "adamw": "hod adamw_vec_kernel (K2)",
     "pack": "hod pack_kernel (K1)",
@@ -331,14 +334,16 @@ def run_ours(args) -> None:
         elems = kbytes / 28 if dom != "rs" else kbytes / (2 * opt.dp + 2)
         per_elem = {"fused": 4, "adamw_ag": 2, "rs": 2}[dom] * (opt.dp - 1)
         nvl = elems * per_elem / (ktime / 1e3) / 1e9 if ktime > 0 else None
-        roof.update({"bound": "nvlink", "achieved": nvl, "peak": 900.0,
-                     "frac": nvl / 900.0 if nvl else None, "peak_source": "NVLink 5 nominal 900 GB/s/dir "
-                     "(measured peer copy 770 GB/s, B200_PROFILING.md)",
+        roof.update({"bound": "nvlink", "achieved": nvl, "peak": NVLINK_MEASURED,
+                     "frac": nvl / NVLINK_MEASURED if nvl else None,
+                     "peak_source": "NVLink 5 measured peer copy 770 GB/s/dir (B200_PROFILING.md); "
+                     "nominal 900 in frac_nominal",
+                     "frac_nominal": nvl / NVLINK_NOMINAL if nvl else None,
                      "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak if achieved else None},
                      "nvlink_bytes_per_owned_element": per_elem})
     kernels = {k: {"launches": n, "ms_total": t, "GBps": (b / (t / 1e3)) / 1e9 if t else None}
                for k, (n, t, b) in kt.items()}
-    # step-level roofline: max(HBM bytes / peak, NVLink bytes / 900 GB/s)
+    # step-level roofline: max(HBM bytes / peak, NVLink bytes / link bandwidth)
     d = opt.dp
     P = gs.total  # this rank's stage
     src_b = 4 if gdtype == torch.float32 else 2
@@ -347,10 +352,15 @@ def run_ours(args) -> None:
     else:
         hbm_bytes = (src_b + 2) * P + 28 * P / d + (2 * P / d if clip else 0)
     nvl_bytes = 4 * P * (d - 1) / d
-    t_roof = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / 900e9), world)
+    # NVLink denominator: the measured 770 GB/s/dir peer copy (B200_PROFILING.md);
+    # the nominal-900 roofline (BASELINE.md's table) is reported beside it
+    t_roof = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / (NVLINK_MEASURED * 1e9)), world)
+    t_roof_nom = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / (NVLINK_NOMINAL * 1e9)), world)
     step_roof = {"t_roof_ms": t_roof * 1e3, "frac": (t_roof * 1e3) / ms,
+                 "t_roof_nominal_ms": t_roof_nom * 1e3, "frac_nominal": (t_roof_nom * 1e3) / ms,
                  "hbm_bytes_per_gpu": hbm_bytes, "nvlink_bytes_per_gpu_per_dir": nvl_bytes,
-                 "bound": "hbm" if hbm_bytes / (peak * 1e9) >= nvl_bytes / 900e9 else "nvlink"}
+                 "nvlink_peak_gbps": NVLINK_MEASURED,
+                 "bound": "hbm" if hbm_bytes / (peak * 1e9) >= nvl_bytes / (NVLINK_MEASURED * 1e9) else "nvlink"}
 
     # ---- e2e through the public API with host buffers ---------------------
     e2e = None

@@ -235,6 +235,9 @@ int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg,
                  unsigned long long timeout_ns, uint32_t* err, float max_norm, float* coef,
                  float* norm, float* sumsq, void* stream);
 
+/* ---- copy-engine transfer (peer-mapped addresses, no SMs used) ---------- */
+int hod_ce_copy(void* dst, const void* src, size_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,7 @@ EXPORTED = (
     "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
-    "hod_p2p_step", "hod_p2p_barrier", "hod_p2p_norm", "hod_p2p_signal", "hod_p2p_wait",
+    "hod_p2p_step", "hod_p2p_barrier", "hod_p2p_norm", "hod_p2p_signal", "hod_p2p_wait", "hod_ce_copy",
 )
 
 
@@ -106,6 +106,7 @@ def load(build_if_missing: bool = True):
         "hod_p2p_step": ([ctypes.POINTER(P2PSpan), I, ctypes.POINTER(AdamWParams), P], I),
         "hod_p2p_barrier": ([P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, P], I),
         "hod_p2p_norm": ([P, I64, P, P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, F, P, P, P, P], I),
+        "hod_ce_copy": ([P, P, ctypes.c_size_t, P], I),
         "hod_p2p_signal": ([P, ctypes.c_uint32, P], I),
         "hod_p2p_wait": ([P, ctypes.c_uint32, ctypes.c_ulonglong, P, P], I),
     }

@@ -9,8 +9,8 @@ Executes the flush-synchronised 1F1B schedule the reference SIMULATES
 * each PP row (``build_pp`` Eq. 2, groups.py:126-134) is a symmetric-memory
   group; every rank owns receive slots ``fwd_in[k]`` / ``bwd_in[k]`` for the
   m micro-batches of an iteration and a flag per slot;
-* a send is a device copy into the neighbour's slot followed by
-  ``hod_p2p_signal`` (system fence + release store of the iteration epoch);
+* a send is a copy-engine transfer (``hod_ce_copy``) into the neighbour's
+  slot followed by ``hod_p2p_signal`` (system fence + release store of the iteration epoch);
   a receive is ``hod_p2p_wait`` on the local flag before the consumer runs —
   sends never block (one slot per micro-batch), so the 1F1B order cannot
   deadlock the way paired blocking send/recv can;
@@ -97,7 +97,11 @@ class PipelineRunner:
         """kind 0: activation to the next stage; 1: gradient to the previous one."""
         q = self.pos + 1 if kind == 0 else self.pos - 1
         dst = self._slot(self.fwd_in if kind == 0 else self.bwd_in, q, k)
-        dst.copy_(t, non_blocking=True)
+        # copy engine over NVLink (one peer: ~0.75 TB/s, tools/ce_probe.py); no
+        # SM leaves the stage's GEMMs for the hand-off
+        t = t.contiguous()
+        nat.call("hod_ce_copy", dst.data_ptr(), t.data_ptr(), t.numel() * t.element_size(),
+                 nat.stream_ptr(self.stream))
         nat.call("hod_p2p_signal", self._flag_ptr(q, kind, k), self.epoch, nat.stream_ptr(self.stream))
 
     def _recv(self, kind: int, k: int) -> torch.Tensor:
