@@ -145,6 +145,18 @@ int hod_adamw_tma(float* master, float* exp_avg, float* exp_avg_sq, const uint16
                   uint16_t* param, int64_t n, const hod_adamw_params* hp, const float* clip_coef,
                   int max_ctas, void* stream);
 
+/* The SURVEY §8b scalar-argument spelling of K2 (same kernel, same bits as
+ * hod_adamw_bf16 with hp = {lr, beta1, beta2, eps, weight_decay, step}). */
+int hod_adamw(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* grad,
+              uint16_t* param, int64_t n, float lr, float beta1, float beta2, float eps,
+              float weight_decay, int64_t step, const float* clip_coef, void* stream);
+
+/* The SURVEY §8b accumulating spelling of K3: *out += sum(x^2) (fp32 result of
+ * the fixed-grid partials summed in fixed order, so bit-reproducible).  Uses a
+ * per-device scratch array inside the library: calls on two streams of one
+ * device must not run concurrently (use hod_sumsq_bf16 + caller partials then). */
+int hod_sumsq(const uint16_t* x, int64_t n, float* out, void* stream);
+
 /* Same update reading an fp32 gradient (fp32 reduce-scatter parity mode). */
 int hod_adamw_f32(float* master, float* exp_avg, float* exp_avg_sq,
                   const float* grad, uint16_t* param, int64_t n,

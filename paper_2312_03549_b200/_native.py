@@ -24,7 +24,7 @@ HOD_DTYPE_F32 = 1
 EXPORTED = (
     "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
     "hod_pack_bf16", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
-    "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma",
+    "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma", "hod_adamw", "hod_sumsq",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
     "hod_p2p_step", "hod_p2p_barrier", "hod_p2p_norm", "hod_p2p_signal", "hod_p2p_wait", "hod_ce_copy",
@@ -95,6 +95,8 @@ def load(build_if_missing: bool = True):
         "hod_pack_sumsq": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, P], I),
         "hod_clip_coef": ([P, F, P, P, P], I),
         "hod_adamw_bf16": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
+        "hod_adamw": ([P, P, P, P, P, I64, F, F, F, F, F, I64, P, P], I),
+        "hod_sumsq": ([P, I64, P, P], I),
         "hod_adamw_f32": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
         "hod_adamw_tma": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, I, P], I),
         "hod_nccl_unique_id": ([P], I),

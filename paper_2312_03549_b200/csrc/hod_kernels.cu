@@ -406,6 +406,17 @@ __global__ void sum_partials_kernel(const float* __restrict__ partials, int64_t 
   if (threadIdx.x == 0) *out = static_cast<float>(acc);
 }
 
+// scratch of hod_sumsq (module-static: no runtime allocation by the library)
+__device__ float g_sumsq_scratch[HOD_SUMSQ_PARTIALS];
+
+__global__ void accumulate_partials_kernel(const float* __restrict__ partials, int64_t n, float* out) {
+  double acc = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 32) acc += static_cast<double>(partials[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (threadIdx.x == 0) *out = __fadd_rn(*out, static_cast<float>(acc));
+}
+
 __global__ void clip_coef_kernel(const float* sumsq, float max_norm, float* coef, float* norm) {
   const float nrm = __fsqrt_rn(*sumsq);
   const float c = __fdiv_rn(max_norm, __fadd_rn(nrm, 1e-6f));
@@ -556,6 +567,26 @@ int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) 
   count_launch(1);
   sumsq_kernel<<<partials_grid(), kSumsqThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
   return cuda_status(cudaGetLastError(), "hod_sumsq_bf16 launch");
+}
+
+int hod_sumsq(const uint16_t* x, int64_t n, float* out, void* stream) {
+  if (!out || n < 0 || (n > 0 && !x)) { set_error("hod_sumsq: bad arguments"); return HOD_EINVAL; }
+  float* scratch = nullptr;
+  int rc = cuda_status(cudaGetSymbolAddress(reinterpret_cast<void**>(&scratch), g_sumsq_scratch),
+                       "hod_sumsq scratch");
+  if (rc) return rc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  count_launch(2);
+  sumsq_kernel<<<partials_grid(), kSumsqThreads, 0, s>>>(x, n, aligned16(x), scratch);
+  accumulate_partials_kernel<<<1, 32, 0, s>>>(scratch, HOD_SUMSQ_PARTIALS, out);
+  return cuda_status(cudaGetLastError(), "hod_sumsq launch");
+}
+
+int hod_adamw(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* grad, uint16_t* param,
+              int64_t n, float lr, float beta1, float beta2, float eps, float weight_decay, int64_t step,
+              const float* clip_coef, void* stream) {
+  const hod_adamw_params hp{lr, beta1, beta2, eps, weight_decay, step};
+  return hod_adamw_bf16(master, exp_avg, exp_avg_sq, grad, param, n, &hp, clip_coef, stream);
 }
 
 int hod_sum_partials(const float* partials, int64_t n_partials, float* out, void* stream) {

@@ -455,7 +455,11 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
   const int64_t chunks = (a.elem_end[a.n_buckets - 1] + kChunk - 1) / kChunk;
   // RS keeps a FIXED grid so its sum-of-squares partials are reproducible
   // 2 CTAs/SM measured best for the fused span kernel (tools/sweep_grid.sh, d = 2/4)
-  const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(chunks * 32, kThreads, 2);
+  static const int p2p_cps = [] {
+    const char* e = getenv("HOD_P2P_CTAS_PER_SM");  // tuning override of the fused/AG grid
+    return e ? atoi(e) : 2;
+  }();
+  const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(chunks * 32, kThreads, p2p_cps);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const bool nv = sp->nvls != 0;
   if (mode == HOD_P2P_FUSED) {

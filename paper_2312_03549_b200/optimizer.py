@@ -235,7 +235,10 @@ class DistributedOptimizer:
         # tiles, the optimizer's CTAs are dispatched first
         hi = torch.cuda.Stream.priority_range()[1] if hasattr(torch.cuda.Stream, "priority_range") else -1
         self.s_pack = torch.cuda.Stream(device=dev, priority=hi)
-        self.s_comm = torch.cuda.Stream(device=dev, priority=hi) if self.dp > 1 else self.s_pack
+        # HOD_COMM_PRIORITY_DROP (tuning): the collective stream this many
+        # levels below the pack stream
+        comm_prio = hi + int(os.environ.get("HOD_COMM_PRIORITY_DROP", "0"))
+        self.s_comm = torch.cuda.Stream(device=dev, priority=comm_prio) if self.dp > 1 else self.s_pack
         self.s_opt = torch.cuda.Stream(device=dev, priority=hi) if self.dp > 1 else self.s_pack
         nb = len(L.buckets)
         self._ev_packed = [torch.cuda.Event() for _ in range(nb)]

@@ -202,6 +202,37 @@ def test_pack_sumsq_matches_packed_norm(oracle, native, src_dtype, scale):
         assert abs(a - want) <= 1e-5 * want
 
 
+def test_survey_spellings_match(oracle, native):
+    """hod_adamw (scalar args) and hod_sumsq (accumulating) — the SURVEY §8b
+    spellings — give the same bits as hod_adamw_bf16 / hod_sumsq_bf16."""
+    n = 1_000_003
+    gen = torch.Generator(device=DEV).manual_seed(21)
+    g = (torch.randn(n, generator=gen, device=DEV) * 1e-3).to(torch.bfloat16)
+    st = [torch.randn(n, generator=gen, device=DEV) * 0.02, torch.zeros(n, device=DEV), torch.zeros(n, device=DEV)]
+    st2 = [t.clone() for t in st]
+    p1 = torch.empty(n, dtype=torch.bfloat16, device=DEV)
+    p2 = torch.empty_like(p1)
+    f = [float(np.float32(x)) for x in (1e-4, 0.9, 0.95, 1e-8, 0.1)]
+    hp = nat.AdamWParams(*f, 1)
+    nat.call("hod_adamw_bf16", *[t.data_ptr() for t in st], g.data_ptr(), p1.data_ptr(), n, ctypes.byref(hp), None, 0)
+    nat.call("hod_adamw", *[t.data_ptr() for t in st2], g.data_ptr(), p2.data_ptr(), n, *f, 1, None, 0)
+    torch.cuda.synchronize()
+    for a, b in zip(st + [p1], st2 + [p2]):
+        assert torch.equal(a.view(torch.int32) if a.dtype == torch.float32 else a.view(torch.int16),
+                           b.view(torch.int32) if b.dtype == torch.float32 else b.view(torch.int16))
+    parts = torch.empty(nat.HOD_SUMSQ_PARTIALS, device=DEV)
+    ref = torch.empty(1, device=DEV)
+    nat.call("hod_sumsq_bf16", g.data_ptr(), n, parts.data_ptr(), 0)
+    nat.call("hod_sum_partials", parts.data_ptr(), nat.HOD_SUMSQ_PARTIALS, ref.data_ptr(), 0)
+    acc = torch.zeros(1, device=DEV)
+    nat.call("hod_sumsq", g.data_ptr(), n, acc.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert acc.item() == ref.item()
+    nat.call("hod_sumsq", g.data_ptr(), n, acc.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert acc.item() == 2 * ref.item()
+
+
 def test_bad_arguments_raise_device_error(native):
     from paper_2312_03549_b200.errors import DeviceError
 
