@@ -113,6 +113,19 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
 int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel,
                    float scale, int src_dtype, float* partials, void* stream);
 
+/* ---- K1 + reduce-scatter transfer in one kernel (push) ---------------------
+ * The pack of hod_pack_bf16 with each packed element stored straight into its
+ * OWNER's buffer over NVLink: element i of the bucket (shard q = i / n, n =
+ * bucket_numel / d, a multiple of 8) goes to dst_buckets[q][rank*n + i - q*n],
+ * i.e. slot `rank` of rank q's bucket region.  dst_buckets[q] = the peer-mapped
+ * address of this bucket's start in rank q's flat grad buffer (dst_buckets[rank]
+ * is local).  After every rank's push (and a barrier) each rank reduces its d
+ * slots locally (hod_p2p_span.staged = 1): the RS bytes cross NVLink during the
+ * pack — during backward — instead of in the update kernel. */
+int hod_pack_push(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel,
+                  float scale, int src_dtype, uint16_t* const* dst_buckets, int d, int rank,
+                  void* stream);
+
 /* ---- K3: deterministic sum of squares of a bf16 shard -----
  * Writes HOD_SUMSQ_PARTIALS fp32 partial sums to partials[0..HOD_SUMSQ_PARTIALS)
  * (fixed grid, fixed order => bit-reproducible for a given n). */
@@ -223,6 +236,11 @@ typedef struct hod_p2p_span {
   int slot;               /* barrier slot (index of the span's first bucket) */
   uint32_t epoch;         /* monotonically increasing per step, > 0 */
   unsigned long long timeout_ns; /* barrier spin budget (0 = 20 s) */
+  int staged;             /* 1: the reduce-scatter was pushed by hod_pack_push — slot q of
+                             bucket k's region in local_grad (bucket_start[k] + q*shard_numel[k])
+                             holds rank q's part of this rank's shard; RS/FUSED read the d slots
+                             locally (same rank-order sum, same bits as the pull); grad[] unused.
+                             p2p all-gather only (nvls must be 0). */
 } hod_p2p_span;
 
 int hod_p2p_step(const hod_p2p_span* span, int mode, const hod_adamw_params* hp, void* stream);

@@ -23,7 +23,7 @@ HOD_DTYPE_F32 = 1
 # every symbol include/hod.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
-    "hod_pack_bf16", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
+    "hod_pack_bf16", "hod_pack_push", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
     "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma", "hod_adamw", "hod_sumsq",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
@@ -55,6 +55,7 @@ class P2PSpan(ctypes.Structure):
         ("n_buckets", ctypes.c_int), ("d", ctypes.c_int), ("rank", ctypes.c_int), ("nvls", ctypes.c_int),
         ("keep_reduced", ctypes.c_int), ("slot", ctypes.c_int),
         ("epoch", ctypes.c_uint32), ("timeout_ns", ctypes.c_ulonglong),
+        ("staged", ctypes.c_int),
     ]
 
 
@@ -93,6 +94,7 @@ def load(build_if_missing: bool = True):
                             ctypes.POINTER(AdamWParams), P, P], I),
         "hod_sum_partials": ([P, I64, P, P], I),
         "hod_pack_sumsq": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, P], I),
+        "hod_pack_push": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, I, I, P], I),
         "hod_clip_coef": ([P, F, P, P, P], I),
         "hod_adamw_bf16": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
         "hod_adamw": ([P, P, P, P, P, I64, F, F, F, F, F, I64, P, P], I),

@@ -45,6 +45,14 @@ struct PeerTable {
   uintptr_t p[kMaxRanks];
 };
 
+// Where the reduce-scatter reads the d contributions of an owned element:
+enum : int {
+  kSrcPeer = 0,    // pull from the d peers' packed buckets (p2p)
+  kSrcNvls = 1,    // one multimem.ld_reduce through the switch (nvls; AG via multimem.st)
+  kSrcStaged = 2,  // pushed into the local buffer by hod_pack_push (slot q of the
+                   // bucket region holds rank q's part of this rank's shard)
+};
+
 struct BarrierArgs {
   PeerTable flags;          // flags[q] = base of rank q's flag array (device ptrs)
   uint32_t* local_flags;    // this rank's flag array
@@ -65,6 +73,7 @@ struct SpanArgs {
   const float* coef;        // optional clip coefficient (device)
   int64_t own_off[kMaxSpan];     // element offset of this rank's shard of bucket k
   int64_t elem_end[kMaxSpan];    // prefix (inclusive) of shard elements over the span
+  int64_t shard_n[kMaxSpan];     // shard numel of bucket k (staged slot stride)
   int n_buckets;
   int d;
   int keep_reduced;
@@ -144,42 +153,52 @@ __device__ __forceinline__ void st_multicast8(uint16_t* mc, const uint2& q) {
 // Quads never straddle buckets (shards are multiples of 16 elements); each
 // quad is located on its own.  Split into a load phase and a compute/store
 // phase so U items can have all their loads in flight at once.
-template <int D, bool kNVLS>
+template <int D, int kSrc>
 struct Item {
-  static constexpr int kRaw = kNVLS ? 1 : (D > 0 ? D : kMaxRanks);
+  static constexpr int kRaw = kSrc == kSrcNvls ? 1 : (D > 0 ? D : kMaxRanks);
   uint2 raw[2][kRaw];  // per quad: peers' bucket vectors (p2p), the switch-reduced
                        // vector (nvls) or the local reduced shard (mode 2, raw[h][0])
   float4 st[2][3];     // per quad: master, m, v
   int64_t e[2];        // element offset in the flat buffers
   int64_t s[2];        // element offset in the span's state
+  int64_t sn[2];       // shard numel of the quad's bucket (staged slot stride)
   bool ok[2];
 };
 
 // Locate the quad starting at span element f; `k` is the caller's
 // monotonically advancing bucket cursor.
-__device__ __forceinline__ bool locate(const SpanArgs& a, int64_t f, int& k, int64_t& e, int64_t& s) {
+__device__ __forceinline__ bool locate(const SpanArgs& a, int64_t f, int& k, int64_t& e, int64_t& s,
+                                       int64_t& sn) {
   if (f >= a.elem_end[a.n_buckets - 1]) return false;
   while (k < a.n_buckets - 1 && f >= a.elem_end[k]) ++k;
   const int64_t first = k ? a.elem_end[k - 1] : 0;
   e = a.own_off[k] + (f - first);
   s = f;
+  sn = a.shard_n[k];
   return true;
 }
 
-template <int D, bool kNVLS, int kMode>
-__device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kNVLS>& it) {
+template <int D, int kSrc, int kMode>
+__device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kSrc>& it, int rank) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (!it.ok[h]) continue;
     const int64_t e = it.e[h];
     if (kMode == 2) {
       it.raw[h][0] = *reinterpret_cast<const uint2*>(a.local_grad + e);
-    } else if constexpr (kNVLS) {
+    } else if constexpr (kSrc == kSrcNvls) {
       it.raw[h][0] = ld_reduce_bf16x4(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e);
+    } else if constexpr (kSrc == kSrcStaged) {
+      // slot q of the bucket region = e + (q - rank) * shard numel, all local
+      const int dd = D > 0 ? D : a.d;
+      const uint16_t* base = a.local_grad + e - static_cast<int64_t>(rank) * it.sn[h];
+#pragma unroll
+      for (int q = 0; q < Item<D, kSrc>::kRaw; ++q)
+        if (q < dd) it.raw[h][q] = *reinterpret_cast<const uint2*>(base + q * it.sn[h]);
     } else {
       const int dd = D > 0 ? D : a.d;
 #pragma unroll
-      for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q)
+      for (int q = 0; q < Item<D, kSrc>::kRaw; ++q)
         if (q < dd) it.raw[h][q] = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
     }
     if (kMode != 1) {
@@ -190,9 +209,9 @@ __device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kNVLS>& it)
   }
 }
 
-template <int D, bool kNVLS>
+template <int D, int kSrc>
 __device__ __forceinline__ void gather_store4(const SpanArgs& a, int64_t e, const uint2& q4) {
-  if constexpr (kNVLS) {
+  if constexpr (kSrc == kSrcNvls) {
     st_multicast8(reinterpret_cast<uint16_t*>(a.param.p[0]) + e, q4);
   } else {
     const int dd = D > 0 ? D : a.d;
@@ -202,20 +221,20 @@ __device__ __forceinline__ void gather_store4(const SpanArgs& a, int64_t e, cons
   }
 }
 
-template <int D, bool kNVLS, int kMode>
-__device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kNVLS>& it,
+template <int D, int kSrc, int kMode>
+__device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSrc>& it,
                                             const AdamWConsts& c, float coef, float& ss) {
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (!it.ok[h]) continue;
     float g[4];
-    if (kMode == 2 || kNVLS) {
+    if (kMode == 2 || kSrc == kSrcNvls) {
       unpack4(it.raw[h][0], g);
     } else {
       const int dd = D > 0 ? D : a.d;
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int q = 0; q < Item<D, kNVLS>::kRaw; ++q) {
+      for (int q = 0; q < Item<D, kSrc>::kRaw; ++q) {
         if (q < dd) {
           float f[4];
           unpack4(it.raw[h][q], f);
@@ -246,14 +265,14 @@ __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kNV
     *reinterpret_cast<float4*>(a.master + it.s[h]) = make_float4(pf[0], pf[1], pf[2], pf[3]);
     *reinterpret_cast<float4*>(a.m + it.s[h]) = make_float4(mf[0], mf[1], mf[2], mf[3]);
     *reinterpret_cast<float4*>(a.v + it.s[h]) = make_float4(vf[0], vf[1], vf[2], vf[3]);
-    gather_store4<D, kNVLS>(a, it.e[h], pack4(pf));
+    gather_store4<D, kSrc>(a, it.e[h], pack4(pf));
   }
 }
 
 // kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+in-place reduced shard, partials),
 // 2 = AdamW+AG from the in-place reduced shard.  U: items per thread in flight
 // (memory-level parallelism for the NVLink loads).
-template <int D, bool kNVLS, int kMode, int U>
+template <int D, int kSrc, int kMode, int U>
 __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constant__ SpanArgs a,
                                                              const BarrierArgs b, const AdamWConsts c,
                                                              int rank) {
@@ -270,17 +289,18 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constan
   for (int u = 0; u < U; ++u) cur[u] = 0;
   for (int64_t base = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; base < n_chunks;
        base += n_warps * U) {
-    Item<D, kNVLS> it[U];
+    Item<D, kSrc> it[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t ch = base + u * n_warps;
 #pragma unroll
       for (int h = 0; h < 2; ++h)
-        it[u].ok[h] = ch < n_chunks && locate(a, ch * kChunk + h * 128 + lane * 4, cur[u], it[u].e[h], it[u].s[h]);
-      load_item<D, kNVLS, kMode>(a, it[u]);
+        it[u].ok[h] = ch < n_chunks && locate(a, ch * kChunk + h * 128 + lane * 4, cur[u], it[u].e[h], it[u].s[h],
+                                               it[u].sn[h]);
+      load_item<D, kSrc, kMode>(a, it[u], rank);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) finish_item<D, kNVLS, kMode>(a, it[u], c, coef, ss);
+    for (int u = 0; u < U; ++u) finish_item<D, kSrc, kMode>(a, it[u], c, coef, ss);
   }
   if (kMode == 1 && a.partials) {
     const float s = block_sum_f(ss);
@@ -353,7 +373,7 @@ static int unroll_setting() {
   return u;
 }
 
-template <int D, bool kNVLS, int kMode>
+template <int D, int kSrc, int kMode>
 static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWConsts& c, int rank,
                         int grid, cudaStream_t s) {
   count_launch(1);
@@ -361,19 +381,19 @@ static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWCons
   // at d = 2 (one remote load each); at d >= 4 the register cost outweighs it
   const int u = unroll_setting();
   if (u >= 2 || (u == 0 && D == 2))
-    p2p_step_kernel<D, kNVLS, kMode, 2><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+    p2p_step_kernel<D, kSrc, kMode, 2><<<grid, kThreads, 0, s>>>(a, b, c, rank);
   else
-    p2p_step_kernel<D, kNVLS, kMode, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+    p2p_step_kernel<D, kSrc, kMode, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
 }
 
-template <bool kNVLS, int kMode>
+template <int kSrc, int kMode>
 static void dispatch_d(const SpanArgs& a, const BarrierArgs& b, const AdamWConsts& c, int rank,
                        int grid, cudaStream_t s) {
-  switch (kNVLS ? 0 : a.d) {
-    case 2: launch_step<2, kNVLS, kMode>(a, b, c, rank, grid, s); break;
-    case 4: launch_step<4, kNVLS, kMode>(a, b, c, rank, grid, s); break;
-    case 8: launch_step<8, kNVLS, kMode>(a, b, c, rank, grid, s); break;
-    default: launch_step<0, kNVLS, kMode>(a, b, c, rank, grid, s); break;
+  switch (kSrc == kSrcNvls ? 0 : a.d) {
+    case 2: launch_step<2, kSrc, kMode>(a, b, c, rank, grid, s); break;
+    case 4: launch_step<4, kSrc, kMode>(a, b, c, rank, grid, s); break;
+    case 8: launch_step<8, kSrc, kMode>(a, b, c, rank, grid, s); break;
+    default: launch_step<0, kSrc, kMode>(a, b, c, rank, grid, s); break;
   }
 }
 
@@ -402,11 +422,15 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
     return HOD_EINVAL;
   }
   memset(a, 0, sizeof(*a));
+  if (sp->staged && sp->nvls) {
+    set_error("hod_p2p: staged (pushed) reduce-scatter pairs with the p2p all-gather only");
+    return HOD_EINVAL;
+  }
   const int nptr = sp->nvls ? 1 : sp->d;
   for (int q = 0; q < nptr; ++q) {
     a->grad.p[q] = reinterpret_cast<uintptr_t>(sp->grad[q]);
     a->param.p[q] = reinterpret_cast<uintptr_t>(sp->param[q]);
-    if (!a->grad.p[q] || !a->param.p[q] || (a->grad.p[q] & 15) || (a->param.p[q] & 15)) {
+    if ((!sp->staged && !a->grad.p[q]) || !a->param.p[q] || (a->grad.p[q] & 15) || (a->param.p[q] & 15)) {
       set_error("hod_p2p: peer buffer %d null or not 16-byte aligned", q);
       return HOD_EALIGN;
     }
@@ -423,6 +447,7 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
       return HOD_EALIGN;
     }
     a->own_off[k] = sp->bucket_start[k] + static_cast<int64_t>(sp->rank) * n;
+    a->shard_n[k] = n;
     elems += n;
     a->elem_end[k] = elems;
   }
@@ -461,13 +486,20 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
   }();
   const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(chunks * 32, kThreads, p2p_cps);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const bool nv = sp->nvls != 0;
+  // staged RS reads locally; its AG goes peer to peer (p2p stores)
+  const int src = sp->staged ? kSrcStaged : (sp->nvls ? kSrcNvls : kSrcPeer);
   if (mode == HOD_P2P_FUSED) {
-    if (nv) dispatch_d<true, 0>(a, b, c, sp->rank, grid, s); else dispatch_d<false, 0>(a, b, c, sp->rank, grid, s);
+    if (src == kSrcNvls) dispatch_d<kSrcNvls, 0>(a, b, c, sp->rank, grid, s);
+    else if (src == kSrcStaged) dispatch_d<kSrcStaged, 0>(a, b, c, sp->rank, grid, s);
+    else dispatch_d<kSrcPeer, 0>(a, b, c, sp->rank, grid, s);
   } else if (mode == HOD_P2P_RS) {
-    if (nv) dispatch_d<true, 1>(a, b, c, sp->rank, grid, s); else dispatch_d<false, 1>(a, b, c, sp->rank, grid, s);
+    if (src == kSrcNvls) dispatch_d<kSrcNvls, 1>(a, b, c, sp->rank, grid, s);
+    else if (src == kSrcStaged) dispatch_d<kSrcStaged, 1>(a, b, c, sp->rank, grid, s);
+    else dispatch_d<kSrcPeer, 1>(a, b, c, sp->rank, grid, s);
   } else {
-    if (nv) dispatch_d<true, 2>(a, b, c, sp->rank, grid, s); else dispatch_d<false, 2>(a, b, c, sp->rank, grid, s);
+    // the update half never reads the grad side: only the AG flavour matters
+    if (src == kSrcNvls) dispatch_d<kSrcNvls, 2>(a, b, c, sp->rank, grid, s);
+    else dispatch_d<kSrcPeer, 2>(a, b, c, sp->rank, grid, s);
   }
   return cuda_status(cudaGetLastError(), "hod_p2p_step launch");
 }
