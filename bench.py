@@ -46,6 +46,7 @@ NVLINK_NOMINAL = 900.0    # NVLink 5, 18 links
 KERNEL_NAMES = {
     "adamw": "hod adamw_vec_kernel (K2)",
     "pack": "hod pack_kernel (K1)",
+    "pack_push": "hod pack_push_kernel (K1 + RS transfer over NVLink)",
     "pack_adamw": "hod pack_adamw_kernel (K1+K2 fused, d=1)",
     "fused": "hod p2p_step_kernel FUSED (barrier+RS+AdamW+AG)",
     "rs": "hod p2p_step_kernel RS (+sumsq)",

@@ -203,8 +203,6 @@ __global__ void __launch_bounds__(kThreads) pack_push_kernel(const __grid_consta
 // result is bit-identical to pack followed by AdamW while the 2+2 B/element
 // bucket round trip disappears (28 B/element instead of 32).
 // ---------------------------------------------------------------------------
-constexpr int kFusedTile = kThreads * 8;
-
 template <typename SrcT, bool kClip>
 __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
     const __grid_constant__ PackTable t, int64_t numel, float scale, float* __restrict__ p,

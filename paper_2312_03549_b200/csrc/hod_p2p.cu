@@ -74,6 +74,7 @@ struct SpanArgs {
   int64_t own_off[kMaxSpan];     // element offset of this rank's shard of bucket k
   int64_t elem_end[kMaxSpan];    // prefix (inclusive) of shard elements over the span
   int64_t shard_n[kMaxSpan];     // shard numel of bucket k (staged slot stride)
+  int64_t chunk_end[kMaxSpan];   // prefix (inclusive) of 256-element chunks per bucket shard
   int n_buckets;
   int d;
   int keep_reduced;
@@ -165,17 +166,31 @@ struct Item {
   bool ok[2];
 };
 
-// Locate the quad starting at span element f; `k` is the caller's
-// monotonically advancing bucket cursor.
-__device__ __forceinline__ bool locate(const SpanArgs& a, int64_t f, int& k, int64_t& e, int64_t& s,
-                                       int64_t& sn) {
-  if (f >= a.elem_end[a.n_buckets - 1]) return false;
-  while (k < a.n_buckets - 1 && f >= a.elem_end[k]) ++k;
-  const int64_t first = k ? a.elem_end[k - 1] : 0;
-  e = a.own_off[k] + (f - first);
-  s = f;
-  sn = a.shard_n[k];
-  return true;
+// Locate the two quads of this lane in warp chunk `ch`.  Chunks are counted
+// per bucket shard (a chunk never straddles buckets), so the bucket lookup is
+// warp-uniform and done once per chunk; `k` is the caller's monotonically
+// advancing bucket cursor.  A quad past the shard end (last, partial chunk)
+// is marked !ok (shards are multiples of 16, so quads are all-in or all-out).
+template <typename ItemT>
+__device__ __forceinline__ void locate_chunk(const SpanArgs& a, int64_t ch, int lane, int& k, ItemT& it) {
+  if (ch >= a.chunk_end[a.n_buckets - 1]) {
+    it.ok[0] = it.ok[1] = false;
+    return;
+  }
+  while (k < a.n_buckets - 1 && ch >= a.chunk_end[k]) ++k;
+  const int64_t first_chunk = k ? a.chunk_end[k - 1] : 0;
+  const int64_t first_elem = k ? a.elem_end[k - 1] : 0;
+  const int64_t n = a.shard_n[k];
+  const int64_t own = a.own_off[k];
+  const int64_t base = (ch - first_chunk) * kChunk + lane * 4;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int64_t off = base + h * 128;
+    it.ok[h] = off < n;
+    it.e[h] = own + off;
+    it.s[h] = first_elem + off;
+    it.sn[h] = n;
+  }
 }
 
 template <int D, int kSrc, int kMode>
@@ -280,7 +295,7 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constan
     if (!cross_gpu_barrier(b, a.d, rank)) return;
   }
   const float coef = (kMode == 2 && a.coef) ? __ldg(a.coef) : 1.0f;
-  const int64_t n_chunks = (a.elem_end[a.n_buckets - 1] + kChunk - 1) / kChunk;
+  const int64_t n_chunks = a.chunk_end[a.n_buckets - 1];
   const int64_t n_warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
   const int lane = threadIdx.x & 31;
   float ss = 0.0f;
@@ -293,10 +308,7 @@ __global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constan
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t ch = base + u * n_warps;
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        it[u].ok[h] = ch < n_chunks && locate(a, ch * kChunk + h * 128 + lane * 4, cur[u], it[u].e[h], it[u].s[h],
-                                               it[u].sn[h]);
+      locate_chunk(a, ch, lane, cur[u], it[u]);
       load_item<D, kSrc, kMode>(a, it[u], rank);
     }
 #pragma unroll
@@ -448,6 +460,7 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
     }
     a->own_off[k] = sp->bucket_start[k] + static_cast<int64_t>(sp->rank) * n;
     a->shard_n[k] = n;
+    a->chunk_end[k] = (k ? a->chunk_end[k - 1] : 0) + (n + kChunk - 1) / kChunk;
     elems += n;
     a->elem_end[k] = elems;
   }
@@ -477,7 +490,7 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
   if (mode != HOD_P2P_RS && (!hp || hp->step < 1)) { set_error("hod_p2p_step: bad hp/step"); return HOD_EINVAL; }
   if (mode != HOD_P2P_RS && (!a.master || !a.m || !a.v)) { set_error("hod_p2p_step: null state"); return HOD_EINVAL; }
   const AdamWConsts c = (mode != HOD_P2P_RS) ? fold_adamw(*hp) : AdamWConsts{};
-  const int64_t chunks = (a.elem_end[a.n_buckets - 1] + kChunk - 1) / kChunk;
+  const int64_t chunks = a.chunk_end[a.n_buckets - 1];
   // RS keeps a FIXED grid so its sum-of-squares partials are reproducible
   // 2 CTAs/SM measured best for the fused span kernel (tools/sweep_grid.sh, d = 2/4)
   static const int p2p_cps = [] {

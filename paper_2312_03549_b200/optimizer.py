@@ -123,7 +123,8 @@ class DistributedOptimizer:
                  device=None, param_align: int = 64, process_group=None, norm_group=None,
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
                  sm_budget: int | None = None, span_numel: int = 128 * 2**20,
-                 param_barriers: bool = True, pre_barrier: bool | None = None):
+                 param_barriers: bool = True, pre_barrier: bool | None = None,
+                 rs_push: bool | None = None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -178,6 +179,13 @@ class DistributedOptimizer:
             pre_barrier = env == "1"
         self._pre_barrier_auto = pre_barrier is None
         self.pre_barrier = bool(pre_barrier)
+        # p2p reduce-scatter by PUSH (hod_pack_push: the pack stores each
+        # element into its owner's slot over NVLink, the span kernel reduces
+        # locally) instead of PULL (pack locally, span kernel loads from peers)
+        env = os.environ.get("HOD_RS_PUSH")
+        if env is not None:
+            rs_push = env == "1"
+        self.rs_push = bool(rs_push) if rs_push is not None else False
         self._pending_span: list[int] = []
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
@@ -468,9 +476,15 @@ class DistributedOptimizer:
             self._deferred_pa.append((bi, entries, dtype))
             return
         t0 = self._timed_event(self.s_pack)
-        nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
-                 ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
-        self._timed_close("pack", t0, self.s_pack, (src_bytes + 2) * b.numel)
+        if self.backend == "p2p" and self.rs_push:
+            dsts = (ctypes.c_void_p * self.dp)(*[self._sym_grad.peer(q) + 2 * b.start for q in range(self.dp)])
+            nat.call("hod_pack_push", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale), dtype,
+                     dsts, self.dp, self.shard_index, nat.stream_ptr(self.s_pack))
+            self._timed_close("pack_push", t0, self.s_pack, (src_bytes + 2) * b.numel)
+        else:
+            nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
+                     ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
+            self._timed_close("pack", t0, self.s_pack, (src_bytes + 2) * b.numel)
         self._ev_packed[bi].record(self.s_pack)
         self._launched[bi] = True
 
@@ -583,6 +597,7 @@ class DistributedOptimizer:
         sp.d, sp.rank, sp.nvls = d, self.shard_index, int(self.backend == "nvls")
         sp.keep_reduced = int(self.keep_reduced)
         sp.slot, sp.epoch, sp.timeout_ns = bis[0], self.step_count, self.timeout_ns
+        sp.staged = int(self.backend == "p2p" and self.rs_push)
         hp = self._hp()
         name = {nat.HOD_P2P_FUSED: "fused", nat.HOD_P2P_RS: "rs", nat.HOD_P2P_ADAMW_AG: "adamw_ag"}[mode]
         # algorithmic bytes per launch: local HBM (state 24 B + own param 2 B +

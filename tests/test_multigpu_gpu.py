@@ -115,6 +115,8 @@ CASES = [
     (8, "toy", "bf16", 2_000_000, 0.0, "p2p"),
     (8, "toy", "bf16", 2_000_000, 1.0, "nvls"),
     (8, "toy", "bf16", 2_000_000, 0.0, "nccl"),
+    (2, "odd", "bf16", 300_000, 0.05, "p2p-push"),  # RS pushed by the pack (hod_pack_push)
+    (4, "toy", "f32", 3_000_000, 0.0, "p2p-push"),
 ]
 
 
@@ -127,7 +129,7 @@ def test_multi_rank_parity(oracle, tmp_path, n, config, gd, bucket, clip, backen
     # p2p: deterministic rank-order fp32 sum -> bit-exact; NCCL ring (d > 2) and
     # the NVSwitch reduction order are checked against the fp64 sum bound
     check(oracle, tmp_path, n, config, gd, 2, clip > 0,
-          exact_rs=(backend == "p2p" or (backend == "nccl" and n == 2)))
+          exact_rs=(backend.startswith("p2p") or (backend == "nccl" and n == 2)))
 
 
 MINI_PP_SCENARIO = {
