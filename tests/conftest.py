@@ -18,6 +18,16 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "reference: needs /root/reference (this container only)")
 
 
+def free_port() -> int:
+    """A TCP port the OS reports free on 127.0.0.1 (rendezvous for a test's
+    process group; random picks can hit ports held by earlier NCCL sockets)."""
+    import socket
+
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def cuda_ok() -> bool:
     try:
         import torch

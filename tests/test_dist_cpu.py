@@ -7,7 +7,6 @@
 """
 
 import os
-import random
 from pathlib import Path
 
 import pytest
@@ -20,6 +19,7 @@ from paper_2312_03549_b200.buckets import build_bucket_layout
 from paper_2312_03549_b200.comm import DPGroup, comm_key, exchange_unique_id
 from paper_2312_03549_b200.gradsets import odd_tensors
 from paper_2312_03549_b200.optimizer import fill_master_shards
+from conftest import free_port  # noqa: E402
 
 ROOT = Path(__file__).resolve().parent.parent
 
@@ -59,7 +59,7 @@ def _worker(rank, world, port, result_dir):
 
 
 def test_gloo_world2_bootstrap_and_shards(tmp_path):
-    port = random.randint(41000, 49000)
+    port = free_port()
     mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
     assert (tmp_path / "ok.pt").exists()
 

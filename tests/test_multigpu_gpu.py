@@ -3,7 +3,6 @@ host against the oracle.  Launches tests/mp_worker.py under torch.distributed.ru
 Skipped when the box has fewer GPUs than the case needs."""
 
 import json
-import random
 import subprocess
 import sys
 from pathlib import Path
@@ -14,6 +13,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
+from conftest import free_port  # noqa: E402
 from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
 from paper_2312_03549_b200.synthetic import make_grads  # noqa: E402
 
@@ -35,7 +35,7 @@ def _ulp_bf16(x):
 
 def run_workers(tmp_path, n, **kw):
     args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-            "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
             str(ROOT / "tests" / "mp_worker.py"), "--out", str(tmp_path)]
     for k, v in kw.items():
         args += [f"--{k.replace('_', '-')}", str(v)]
@@ -157,7 +157,7 @@ def test_pp_dp_scenario_parity(oracle, tmp_path, backend, clip):
     scen = tmp_path / "mini_pp.json"
     scen.write_text(json.dumps(MINI_PP_SCENARIO))
     args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
-            "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
             str(ROOT / "tests" / "mp_worker_scenario.py"), "--scenario", str(scen), "--out", str(tmp_path),
             "--clip", str(clip), "--backend", backend]
     r = subprocess.run(args, capture_output=True, text=True, timeout=600)
@@ -209,7 +209,7 @@ def test_pipeline_1f1b_handoffs_over_peer_memory(tmp_path):
     scen = tmp_path / "mini_pp.json"
     scen.write_text(json.dumps(MINI_PP_SCENARIO))
     args = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=4",
-            "--master-addr=127.0.0.1", f"--master-port={random.randint(20000, 40000)}",
+            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
             str(ROOT / "tests" / "mp_worker_pipeline.py"), "--scenario", str(scen), "--out", str(tmp_path),
             "--micro", "4", "--iters", "2"]
     r = subprocess.run(args, capture_output=True, text=True, timeout=600)
