@@ -23,7 +23,8 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 OURS = re.compile(r"hod::|pack_kernel|adamw_vec_kernel|adamw_scalar_kernel|sumsq_kernel|p2p_step_kernel|"
-                  r"barrier_kernel|norm_exchange_kernel|sum_partials_kernel|clip_coef_kernel|pack_adamw")
+                  r"barrier_kernel|norm_exchange_kernel|sum_partials_kernel|clip_coef_kernel|pack_adamw|pack_sumsq|"
+                  r"pack_push|accumulate_partials")
 
 
 def short(name: str) -> str:
@@ -104,7 +105,8 @@ def main():
     doc = {"round": a.round, "note": a.note, "kernels": {}}
     if a.launches:
         doc["launch_list"] = launches(Path(a.launches))
-    spec = {"adamw": (14, 14, 28), "pack": (2, 2, 4), "pack_adamw": (14, 14, 28), "fused": (None, None, 28)}
+    spec = {"adamw": (14, 14, 28), "pack": (2, 2, 4), "pack_adamw": (14, 14, 28), "fused": (None, None, 28),
+            "pack_sumsq": (2, None, 2), "fused_emulated_d2": (None, None, None)}
     for item in a.rep:
         name, path = item.split("=", 1)
         rd, wr, alg = spec.get(name, (None, None, None))
