@@ -350,6 +350,8 @@ def run_ours(args) -> None:
     src_b = 4 if gdtype == torch.float32 else 2
     if d == 1 and not clip:   # K1+K2 fuse: grad read + 24 B state + 2 B param, no bucket
         hbm_bytes = (src_b + 26) * P
+    elif d == 1:              # norm pass over the tensors, then the fused update
+        hbm_bytes = src_b * P + (src_b + 26) * P
     else:
         hbm_bytes = (src_b + 2) * P + 28 * P / d + (2 * P / d if clip else 0)
     nvl_bytes = 4 * P * (d - 1) / d

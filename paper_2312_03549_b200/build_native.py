@@ -54,6 +54,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
         "-Xptxas", "-v" if verbose else "-O3",
         f"-I{inc}", f"-I{ROOT / 'include'}",
+        *os.environ.get("HOD_NVCC_EXTRA", "").split(),   # tuning builds, e.g. -DHOD_P2P_MINB=3
         *srcs,
         f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}",
         "-o", str(LIB),

@@ -145,6 +145,34 @@ int grid_limit();
 // HOD_CTAS_PER_SM (env) overrides the per-kernel CTAs-per-SM cap (tuning runs).
 int ctas_per_sm_override();
 
+// Programmatic dependent launch for back-to-back bucket kernels (HOD_PDL=0 disables).
+bool pdl_enabled();
+
+// Device side: let the next PDL launch in the stream start while this grid
+// drains.  Only for kernels whose successor never reads what they write
+// (consecutive buckets: disjoint memory).
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Host side: launch with programmatic stream serialization, so the kernel may
+// overlap the tail of the previous kernel in the stream IF that kernel called
+// pdl_trigger(); after any other kernel the usual full dependency holds.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
 inline int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 8) {
   int64_t need = (work_items + per_block - 1) / per_block;
   if (ctas_per_sm_override() > 0) max_blocks_per_sm = ctas_per_sm_override();

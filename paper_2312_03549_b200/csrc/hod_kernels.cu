@@ -24,6 +24,14 @@ void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 static thread_local int g_grid_limit = 0;
 int grid_limit() { return g_grid_limit; }
 
+bool pdl_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("HOD_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+
 int ctas_per_sm_override() {
   static const int v = [] {
     const char* e = getenv("HOD_CTAS_PER_SM");
@@ -105,6 +113,7 @@ template <typename SrcT>
 __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ PackTable t,
                                                          uint16_t* __restrict__ dst,
                                                          int64_t bucket_numel, float scale) {
+  pdl_trigger();  // the next bucket's pack touches disjoint memory
   const int64_t n_tiles = (bucket_numel + kPackTile - 1) / kPackTile;
   int e = 0;  // entry cursor; tiles visited by a CTA are increasing
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -163,6 +172,7 @@ template <typename SrcT>
 __global__ void __launch_bounds__(kThreads) pack_push_kernel(const __grid_constant__ PackTable t,
                                                               const __grid_constant__ PushArgs pa,
                                                               int64_t span, float scale) {
+  pdl_trigger();
   const int64_t n_tiles = (span + kPackTile - 1) / kPackTile;
   int e = 0;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
@@ -208,6 +218,7 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
     const __grid_constant__ PackTable t, int64_t numel, float scale, float* __restrict__ p,
     float* __restrict__ m, float* __restrict__ v, uint16_t* __restrict__ out, const AdamWConsts c,
     const float* __restrict__ coef_ptr) {
+  pdl_trigger();  // the next bucket's update touches disjoint memory
   const float coef = kClip ? __ldg(coef_ptr) : 1.0f;
   // warp-strided 256-element chunks (same mapping as adamw_vec_kernel); the
   // table lookup is warp-uniform and the cursor only moves forward
@@ -404,6 +415,7 @@ __global__ void __launch_bounds__(kSumsqThreads) pack_sumsq_kernel(const __grid_
                                                                     float* __restrict__ partials) {
   constexpr int kThreads = kSumsqThreads;
   constexpr int kPackTile = kSumsqTile;
+  pdl_trigger();  // the next bucket's norm pass writes other partial slots
   // 8 independent accumulators (one per vector lane), folded in a fixed order
   // at the end: breaks the serial FADD chain, stays reproducible
   float acc8[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
@@ -562,9 +574,9 @@ int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket
     const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, src_dtype == HOD_DTYPE_BF16 ? 16 : 3);
     count_launch(1);
     if (src_dtype == HOD_DTYPE_BF16)
-      pack_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
+      launch_pdl(pack_kernel<uint16_t>, grid, kThreads, s, t, bucket + lo, span, scale);
     else
-      pack_kernel<float><<<grid, kThreads, 0, s>>>(t, bucket + lo, span, scale);
+      launch_pdl(pack_kernel<float>, grid, kThreads, s, t, bucket + lo, span, scale);
     return cuda_status(cudaGetLastError(), "hod_pack_bf16 launch");
   });
 }
@@ -597,9 +609,9 @@ int hod_pack_push(const hod_pack_entry* entries, int n_entries, int64_t bucket_n
     const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, src_dtype == HOD_DTYPE_BF16 ? 16 : 3);
     count_launch(1);
     if (src_dtype == HOD_DTYPE_BF16)
-      pack_push_kernel<uint16_t><<<grid, kThreads, 0, s>>>(t, pa, span, scale);
+      launch_pdl(pack_push_kernel<uint16_t>, grid, kThreads, s, t, pa, span, scale);
     else
-      pack_push_kernel<float><<<grid, kThreads, 0, s>>>(t, pa, span, scale);
+      launch_pdl(pack_push_kernel<float>, grid, kThreads, s, t, pa, span, scale);
     return cuda_status(cudaGetLastError(), "hod_pack_push launch");
   });
 }
@@ -621,9 +633,16 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
     // 3 CTAs/SM measured best for this kernel (2: -9 %, 4: -9 %; tools/sweep_grid.sh)
     const int grid = grid_for((span + kChunk - 1) / kChunk * 32, kThreads, 3);
     count_launch(1);
+    // PDL: may overlap the tail of the previous kernel in the stream only if
+    // that kernel triggered early — our own bucket kernels (disjoint memory);
+    // anything else (clip_coef_kernel writing the coefficient read here)
+    // triggers at completion, so that dependency holds
+    float* mp = master + lo;
+    float* ep = exp_avg + lo;
+    float* vp = exp_avg_sq + lo;
+    uint16_t* pp = param + lo;
 #define HOD_PA_LAUNCH(T, CLIP) \
-    pack_adamw_kernel<T, CLIP><<<grid, kThreads, 0, s>>>(t, span, scale, master + lo, exp_avg + lo, \
-                                                        exp_avg_sq + lo, param + lo, c, clip_coef)
+    launch_pdl(pack_adamw_kernel<T, CLIP>, grid, kThreads, s, t, span, scale, mp, ep, vp, pp, c, clip_coef)
     if (src_dtype == HOD_DTYPE_BF16) {
       if (clip_coef) HOD_PA_LAUNCH(uint16_t, true); else HOD_PA_LAUNCH(uint16_t, false);
     } else {
@@ -646,9 +665,9 @@ int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_
                          [&](const PackTable& t, int64_t lo, int64_t span) {
     count_launch(1);
     if (src_dtype == HOD_DTYPE_BF16)
-      pack_sumsq_kernel<uint16_t><<<partials_grid(), kSumsqThreads, 0, s>>>(t, span, scale, partials);
+      launch_pdl(pack_sumsq_kernel<uint16_t>, partials_grid(), kSumsqThreads, s, t, span, scale, partials);
     else
-      pack_sumsq_kernel<float><<<partials_grid(), kSumsqThreads, 0, s>>>(t, span, scale, partials);
+      launch_pdl(pack_sumsq_kernel<float>, partials_grid(), kSumsqThreads, s, t, span, scale, partials);
     (void)lo;
     return cuda_status(cudaGetLastError(), "hod_pack_sumsq launch");
   });

@@ -40,6 +40,9 @@ namespace hod {
 
 constexpr int kMaxRanks = HOD_P2P_MAX_RANKS;
 constexpr int kMaxSpan = HOD_P2P_MAX_SPAN;
+#ifndef HOD_P2P_MINB
+#define HOD_P2P_MINB 1
+#endif
 
 struct PeerTable {
   uintptr_t p[kMaxRanks];
@@ -288,7 +291,7 @@ __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSr
 // 2 = AdamW+AG from the in-place reduced shard.  U: items per thread in flight
 // (memory-level parallelism for the NVLink loads).
 template <int D, int kSrc, int kMode, int U>
-__global__ void __launch_bounds__(kThreads) p2p_step_kernel(const __grid_constant__ SpanArgs a,
+__global__ void __launch_bounds__(kThreads, HOD_P2P_MINB) p2p_step_kernel(const __grid_constant__ SpanArgs a,
                                                              const BarrierArgs b, const AdamWConsts c,
                                                              int rank) {
   if (kMode != 2) {

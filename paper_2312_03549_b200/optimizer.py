@@ -42,6 +42,10 @@ from .buckets import BucketLayout, build_bucket_layout
 from .comm import DPGroup, NcclComm
 from .errors import InfeasibleConfigError
 
+# fused pack+AdamW launches are chained with programmatic dependent launch
+# unless HOD_PDL=0 (read by the library too, csrc/hod_kernels.cu)
+_PDL = os.environ.get("HOD_PDL", "1") != "0"
+
 _BF16 = torch.bfloat16
 BACKENDS = ("none", "nccl", "p2p", "nvls")
 
@@ -290,6 +294,8 @@ class DistributedOptimizer:
             dist.barrier()  # every rank's zeroed flags exist before anyone signals
 
         self._ktiming = None
+        self._krun = None                # open run of PDL-chained launches (timing)
+        self._grads_resident = False
         self._staging = None
         self.step_count = 0
         self._pending_grads: list[dict[int, torch.Tensor]] = []
@@ -349,6 +355,7 @@ class DistributedOptimizer:
             self._clip_and_update()
         else:
             self._flush_deferred_ag()
+        self._close_run()
         cur = torch.cuda.current_stream(self.device)
         if wait:
             for ev in self._ev_params:
@@ -370,6 +377,20 @@ class DistributedOptimizer:
         if host:
             self._ensure_staging(grads)
         self.begin_step()
+        if not host:
+            # every gradient is already complete on the current stream: one
+            # wait here instead of one per bucket keeps the pack stream a pure
+            # chain of kernels (programmatic dependent launch can then overlap
+            # bucket k+1's ramp with bucket k's tail)
+            self.s_pack.wait_stream(torch.cuda.current_stream(self.device))
+            self._grads_resident = True
+        try:
+            self._step_buckets(grads, host)
+        finally:
+            self._grads_resident = False
+        return self.finish_step()
+
+    def _step_buckets(self, grads, host: bool) -> None:
         for b in self.layout.buckets:
             if host:
                 # host->device copy of this bucket's gradients on the copy
@@ -381,7 +402,6 @@ class DistributedOptimizer:
                 self.s_pack.wait_event(self._ev_h2d[b.index])
             for s in b.slots:
                 self.grad_ready(s.index, self._staging[s.index] if host else grads[s.index])
-        return self.finish_step()
 
     def _ensure_staging(self, grads) -> None:
         if (self._staging is not None and self._staging[0].dtype == grads[0].dtype):
@@ -434,7 +454,8 @@ class DistributedOptimizer:
         b = self.layout.buckets[bi]
         grads = self._pending_grads[bi]
         cur = torch.cuda.current_stream(self.device)
-        self.s_pack.wait_stream(cur)
+        if not self._grads_resident:
+            self.s_pack.wait_stream(cur)
         # keep gradient memory alive until the pack has consumed it
         for s in b.slots:
             g = grads[s.index]
@@ -469,14 +490,16 @@ class DistributedOptimizer:
                 self._pack_adamw(bi, entries, dtype, None)
                 return
             part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * bi
-            t0 = self._timed_event(self.s_pack)
+            t0 = self._timed_event(self.s_pack, run="pack_sumsq" if self._grads_resident else None)
             nat.call("hod_pack_sumsq", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale),
                      dtype, part, nat.stream_ptr(self.s_pack))
             self._timed_close("pack_sumsq", t0, self.s_pack, src_bytes * b.numel)
             self._deferred_pa.append((bi, entries, dtype))
             return
-        t0 = self._timed_event(self.s_pack)
-        if self.backend == "p2p" and self.rs_push:
+        chained = self._grads_resident   # back-to-back launches: timed as one PDL run
+        push = self.backend == "p2p" and self.rs_push
+        t0 = self._timed_event(self.s_pack, run=("pack_push" if push else "pack") if chained else None)
+        if push:
             dsts = (ctypes.c_void_p * self.dp)(*[self._sym_grad.peer(q) + 2 * b.start for q in range(self.dp)])
             nat.call("hod_pack_push", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale), dtype,
                      dsts, self.dp, self.shard_index, nat.stream_ptr(self.s_pack))
@@ -509,7 +532,8 @@ class DistributedOptimizer:
             # all-gather of the previous bucket goes behind this RS (pipelining)
             self._flush_deferred_ag(keep_last=True)
 
-    def _pack_adamw(self, bi: int, entries, dtype, coef_ptr, last: int | None = None) -> None:
+    def _pack_adamw(self, bi: int, entries, dtype, coef_ptr, last: int | None = None,
+                    chained: bool | None = None) -> None:
         """Fused pack+AdamW (d == 1) over buckets bi..last (default bi): at d = 1
         consecutive buckets are one contiguous range of the flat buffers, so a
         run of them is a single launch (``entries`` offsets relative to bucket bi)."""
@@ -519,7 +543,8 @@ class DistributedOptimizer:
         off = self._shard_off[bi]
         hp = self._hp()
         src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
-        t0 = self._timed_event(self.s_pack)
+        chained = self._grads_resident if chained is None else chained
+        t0 = self._timed_event(self.s_pack, run="pack_adamw" if chained else None)
         nat.call("hod_pack_adamw", entries, len(entries), numel, ctypes.c_float(self.grad_scale),
                  dtype, _ptr(self.master) + 4 * off, _ptr(self.exp_avg) + 4 * off,
                  _ptr(self.exp_avg_sq) + 4 * off, _ptr(self.param_buffer) + 2 * b.start,
@@ -724,7 +749,7 @@ class DistributedOptimizer:
                    and n_ent + len(pend[j][1]) <= nat.HOD_PACK_MAX_ENTRIES):
                 lo, n_ent, j = pend[j][0], n_ent + len(pend[j][1]), j + 1
             if lo == hi:
-                self._pack_adamw(hi, pend[i][1], dtype, coef)
+                self._pack_adamw(hi, pend[i][1], dtype, coef, chained=True)
             else:
                 base = L.buckets[lo].start
                 merged = (nat.PackEntry * n_ent)()
@@ -734,7 +759,7 @@ class DistributedOptimizer:
                     for e in entries:
                         merged[k].src, merged[k].numel, merged[k].dst_offset = e.src, e.numel, e.dst_offset + shift
                         k += 1
-                self._pack_adamw(lo, merged, dtype, coef, last=hi)
+                self._pack_adamw(lo, merged, dtype, coef, last=hi, chained=True)
             i = j
 
     def _clip_and_update(self) -> None:
@@ -760,21 +785,41 @@ class DistributedOptimizer:
         self._ktiming = [] if on else None
 
     def kernel_timing(self) -> dict:
-        """{kernel: (launches, total_ms, algorithmic_bytes)} — synchronises."""
+        """{kernel: (launches, total_ms, algorithmic_bytes)} — synchronises.
+
+        Launches chained by programmatic dependent launch (fused pack+AdamW at
+        d = 1) overlap each other's ramp and tail, so they are timed as one run
+        (events before the first and after the last launch of the run): the
+        run's time divided by its launches is their effective duration."""
+        self._close_run()
         out: dict = {}
-        for name, e0, e1, nbytes in self._ktiming or []:
+        for name, e0, e1, nbytes, nl in self._ktiming or []:
             e1.synchronize()
             n, ms, by = out.get(name, (0, 0.0, 0))
-            out[name] = (n + 1, ms + e0.elapsed_time(e1), by + nbytes)
+            out[name] = (n + nl, ms + e0.elapsed_time(e1), by + nbytes)
         return out
 
     def reset_kernel_timing(self) -> None:
         if self._ktiming is not None:
             self._ktiming = []
 
-    def _timed_event(self, stream):
+    _RUN = object()   # token: launch belongs to the open PDL run
+
+    def _timed_event(self, stream, run: str | None = None):
+        """Start timing a launch.  ``run``: kernel name whose consecutive
+        launches on ``stream`` form one PDL chain — a timing event between them
+        would serialise the chain, so the run gets one start / one end event."""
         if getattr(self, "_ktiming", None) is None:
             return None
+        if run is not None and _PDL:
+            if self._krun is not None and (self._krun[0] != run or self._krun[2] is not stream):
+                self._close_run()
+            if self._krun is None:
+                ev = torch.cuda.Event(enable_timing=True)
+                ev.record(stream)
+                self._krun = [run, ev, stream, 0, 0]
+            return self._RUN
+        self._close_run()
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
         return ev
@@ -782,9 +827,23 @@ class DistributedOptimizer:
     def _timed_close(self, name, e0, stream, nbytes) -> None:
         if e0 is None:
             return
+        if e0 is self._RUN:
+            self._krun[3] += 1
+            self._krun[4] += nbytes
+            return
         e1 = torch.cuda.Event(enable_timing=True)
         e1.record(stream)
-        self._ktiming.append((name, e0, e1, nbytes))
+        self._ktiming.append((name, e0, e1, nbytes, 1))
+
+    def _close_run(self) -> None:
+        if self._krun is None:
+            return
+        name, e0, stream, nl, nbytes = self._krun
+        self._krun = None
+        if nl:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(stream)
+            self._ktiming.append((name, e0, e1, nbytes, nl))
 
     # ------------------------------------------------------------ helpers
     def full_master(self) -> torch.Tensor:

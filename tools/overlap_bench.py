@@ -189,7 +189,8 @@ def main():
     carve(False)
     torch.cuda.synchronize()
     bwd_end_ms = base.elapsed_time(end_bwd)
-    spans = [(name, base.elapsed_time(e0), base.elapsed_time(e1)) for name, e0, e1, _ in opt._ktiming]
+    opt._close_run()
+    spans = [(name, base.elapsed_time(e0), base.elapsed_time(e1)) for name, e0, e1, *_ in opt._ktiming]
     opt.enable_kernel_timing(False)
     busy_in_bwd = sum(max(0.0, min(e, bwd_end_ms) - s0) for _, s0, e in spans if s0 < bwd_end_ms)
     busy_total = sum(e - s0 for _, s0, e in spans)
