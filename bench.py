@@ -430,7 +430,7 @@ def main():
                     help="scenario JSON (reference schema) for a PP x DP run, e.g. "
                          "scenarios/gpt13b_pp2_dp4_hybrid.json (BASELINE config 4, 8 GPUs)")
     ap.add_argument("--bucket-size", type=int, default=25_000_000)
-    ap.add_argument("--span-numel", type=int, default=128 * 2**20,
+    ap.add_argument("--span-numel", type=int, default=256 * 2**20,
                     help="p2p/nvls: coalesce packed buckets into fused launches of >= this many elements")
     ap.add_argument("--backend", default="auto")
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")

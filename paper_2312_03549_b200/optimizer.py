@@ -126,7 +126,7 @@ class DistributedOptimizer:
                  norm_ranks=None, grad_scale: float | None = None, backend: str = "auto",
                  device=None, param_align: int = 64, process_group=None, norm_group=None,
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
-                 sm_budget: int | None = None, span_numel: int = 128 * 2**20,
+                 sm_budget: int | None = None, span_numel: int = 256 * 2**20,
                  param_barriers: bool = True, pre_barrier: bool | None = None,
                  rs_push: bool | None = None):
         if clip is not None and not clip > 0:
