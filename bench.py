@@ -54,6 +54,12 @@ KERNEL_NAMES = {
 }
 
 
+def _desc(cfg, clip) -> str:
+    """Workload text with the clip actually used (``--clip`` may override it)."""
+    base = cfg["desc"].replace(", grad-norm clip 1.0", "")
+    return base + (f", grad-norm clip {clip}" if clip else ", no clip")
+
+
 def _peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -402,7 +408,7 @@ def run_ours(args) -> None:
             "vs_baseline": None, "dtype": "bf16-grads/f32-adamw", "data": "synthetic",
             "config": {"workload": (f"scenario {scen['scenario']}: GPT stages {scen['stage_layers']} "
                                     "(reference self-adapting partition), PP x DP, world clip norm"
-                                    if scen else cfg["desc"]),
+                                    if scen else _desc(cfg, clip)),
                        "config": "scenario" if scen else args.config, "params": params_per_step,
                        "scenario": scen,
                        "buckets": len(opt.layout.buckets), "bucket_size": args.bucket_size,

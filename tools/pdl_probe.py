@@ -23,12 +23,31 @@ m = torch.zeros(N, device=dev)
 v = torch.zeros(N, device=dev)
 out = torch.empty(N, dtype=torch.bfloat16, device=dev)
 hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, 1)
-tables = []
+CLIP = os.environ.get("PROBE_CLIP", "0") == "1"      # pass a clip coefficient (kClip variant)
+MERGE = os.environ.get("PROBE_MERGE", "0") == "1"    # runs of consecutive buckets (<= 64 tensors) per launch
+coef = torch.ones(1, device=dev)
+
+
+class Run:
+    def __init__(self, start, numel, slots):
+        self.start, self.numel, self.slots = start, numel, slots
+
+
+runs = []
 for b in L.buckets:
-    e = (nat.PackEntry * len(b.slots))()
-    for k, s in enumerate(b.slots):
-        e[k].src, e[k].numel, e[k].dst_offset = g.data_ptr() + 2 * (b.start + s.offset), s.numel, s.offset
-    tables.append((b, e))
+    sl = [(b.start + s.offset, s.numel) for s in b.slots]
+    if MERGE and runs and len(runs[-1].slots) + len(sl) <= nat.HOD_PACK_MAX_ENTRIES:
+        r = runs[-1]
+        r.slots += sl
+        r.numel = b.start + b.numel - r.start
+    else:
+        runs.append(Run(b.start, b.numel, sl))
+tables = []
+for r in runs:
+    e = (nat.PackEntry * len(r.slots))()
+    for k, (off, n) in enumerate(r.slots):
+        e[k].src, e[k].numel, e[k].dst_offset = g.data_ptr() + 2 * off, n, off - r.start
+    tables.append((r, e))
 
 
 EVENTS = os.environ.get("PROBE_EVENTS", "0") == "1"   # an event record after every launch
@@ -43,7 +62,7 @@ def step():
             ev0.record()
         nat.call("hod_pack_adamw", e, len(b.slots), b.numel, ctypes.c_float(1.0), nat.HOD_DTYPE_BF16,
                  p.data_ptr() + 4 * b.start, m.data_ptr() + 4 * b.start, v.data_ptr() + 4 * b.start,
-                 out.data_ptr() + 2 * b.start, ctypes.byref(hp), None, 0)
+                 out.data_ptr() + 2 * b.start, ctypes.byref(hp), coef.data_ptr() if CLIP else None, 0)
         if EVENTS or TIMING:
             ev.record()
 
@@ -58,5 +77,5 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
-print(f"HOD_PDL={os.environ.get('HOD_PDL', '1')} events={int(EVENTS)} timing={int(TIMING)} buckets={len(L.buckets)} step {ms:.3f} ms "
+print(f"HOD_PDL={os.environ.get('HOD_PDL', '1')} events={int(EVENTS)} timing={int(TIMING)} clip={int(CLIP)} merge={int(MERGE)} launches={len(runs)} step {ms:.3f} ms "
       f"{28 * N / ms / 1e6:.0f} GB/s (28 B/elem)")
