@@ -14,4 +14,10 @@ for n in 2 4; do
   timeout 900 $TR --master-port 2960$n bench.py --gpus $n --config llama7b > $O/${TAG}_bench_llama_n$n.log 2>&1
 done
 timeout 600 python bench.py --impl reference > $O/${TAG}_bench_reference_n1.log 2>&1
+for n in 2 4; do
+  [ $n -le $N ] || continue
+  TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1"
+  timeout 600 $TR --master-port 2970$n tools/overlap_bench.py --config gpt1.3b --iters 5 2>/dev/null | grep exposed > $O/${TAG}_ovl_gpt_n$n.jsonl
+  timeout 900 $TR --master-port 2980$n tools/overlap_bench.py --config llama7b --clip 1.0 --iters 5 2>/dev/null | grep exposed > $O/${TAG}_ovl_llama_n$n.jsonl
+done
 grep -h '"metric"' $O/${TAG}_bench_*.log | cut -c1-160
