@@ -288,7 +288,9 @@ def run_ours(args) -> None:
         p0 = init_params(gs, dev)
         group = DPGroup(tuple(range(world)), rank)
         opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group,
-                                   backend=args.backend, span_numel=args.span_numel)
+                                   backend=args.backend, span_numel=args.span_numel,
+                                   first_span_numel=args.first_span_numel,
+                                   param_barriers=bool(args.param_barriers))
     del p0
     torch.cuda.empty_cache()
     grads = make_grads(gs, 1, rank, dev, dtype=gdtype)
@@ -336,18 +338,39 @@ def run_ours(args) -> None:
             "avg_launch_ms": ktime / max(1, n_launch), "launches_timed": n_launch,
             "bytes_per_element": 28}
     if dom in ("fused", "adamw_ag", "rs") and opt.dp > 1:
-        # the collective half dominates: report NVLink per direction per GPU
-        # (RS in + AG out for p2p = 2(d-1) B each per owned element)
-        elems = kbytes / 28 if dom != "rs" else kbytes / (2 * opt.dp + 2)
-        per_elem = {"fused": 4, "adamw_ag": 2, "rs": 2}[dom] * (opt.dp - 1)
+        # a collective span kernel: the binding resource is whichever of local
+        # HBM (28 B per owned element for the update; RS: own shard read +
+        # reduced shard write) and NVLink per direction (SURVEY §8d algorithmic
+        # bytes: RS in + AG out = 2(d-1) B each per owned element) needs longer
+        d_ = opt.dp
+        elems = kbytes / 28 if dom != "rs" else kbytes / (2 * d_ + 2)
+        per_elem = {"fused": 4, "adamw_ag": 2, "rs": 2}[dom] * (d_ - 1)
+        hbm_elem = {"fused": 28, "adamw_ag": 28, "rs": 4}[dom]
         nvl = elems * per_elem / (ktime / 1e3) / 1e9 if ktime > 0 else None
-        roof.update({"bound": "nvlink", "achieved": nvl, "peak": NVLINK_MEASURED,
-                     "frac": nvl / NVLINK_MEASURED if nvl else None,
-                     "peak_source": "NVLink 5 measured peer copy 770 GB/s/dir (B200_PROFILING.md); "
-                     "nominal 900 in frac_nominal",
-                     "frac_nominal": nvl / NVLINK_NOMINAL if nvl else None,
-                     "hbm_view": {"achieved": achieved, "peak": peak, "frac": achieved / peak if achieved else None},
-                     "nvlink_bytes_per_owned_element": per_elem})
+        hbm = elems * hbm_elem / (ktime / 1e3) / 1e9 if ktime > 0 else None
+        hbm_view = {"achieved": hbm, "peak": peak, "frac": hbm / peak if hbm else None,
+                    "bytes_per_owned_element": hbm_elem}
+        nvl_view = {"achieved": nvl, "peak": NVLINK_MEASURED, "frac": nvl / NVLINK_MEASURED if nvl else None,
+                    "frac_nominal": nvl / NVLINK_NOMINAL if nvl else None,
+                    "bytes_per_owned_element": per_elem}
+        if opt.backend == "nvls":
+            # what the switch actually moves per GPU and direction (the larger of
+            # egress / ingress): fused 2(d+1), RS egress 2d, AG ingress 2d
+            phys = {"fused": 2 * (d_ + 1), "adamw_ag": 2 * d_, "rs": 2 * d_}[dom]
+            nvl_view["physical_bytes_per_owned_element"] = phys
+            nvl_view["physical_achieved"] = elems * phys / (ktime / 1e3) / 1e9 if ktime > 0 else None
+        if hbm_elem / peak >= per_elem / NVLINK_MEASURED:
+            roof.update({"bound": "hbm", "achieved": hbm, "frac": hbm_view["frac"],
+                         "bytes_per_element": hbm_elem, "nvlink_view": nvl_view})
+        else:
+            roof.update({"bound": "nvlink", "achieved": nvl, "peak": NVLINK_MEASURED, "frac": nvl_view["frac"],
+                         "peak_source": "NVLink 5 measured peer copy 770 GB/s/dir (B200_PROFILING.md); "
+                         "nominal 900 in frac_nominal",
+                         "frac_nominal": nvl_view["frac_nominal"], "hbm_view": hbm_view,
+                         "nvlink_bytes_per_owned_element": per_elem, "bytes_per_element": per_elem})
+            if "physical_achieved" in nvl_view:
+                roof["nvlink_physical"] = {k: nvl_view[k] for k in
+                                           ("physical_bytes_per_owned_element", "physical_achieved")}
     kernels = {k: {"launches": n, "ms_total": t, "GBps": (b / (t / 1e3)) / 1e9 if t else None}
                for k, (n, t, b) in kt.items()}
     # step-level roofline: max(HBM bytes / peak, NVLink bytes / link bandwidth)
@@ -438,6 +461,10 @@ def main():
     ap.add_argument("--bucket-size", type=int, default=25_000_000)
     ap.add_argument("--span-numel", type=int, default=256 * 2**20,
                     help="p2p/nvls: coalesce packed buckets into fused launches of >= this many elements")
+    ap.add_argument("--first-span-numel", type=int, default=None,
+                    help="p2p/nvls: threshold of the step's first span (default: min(--span-numel, 32M))")
+    ap.add_argument("--param-barriers", type=int, default=1, choices=[0, 1],
+                    help="p2p/nvls: params-ready barrier per span (1) or one end-of-step barrier (0)")
     ap.add_argument("--backend", default="auto")
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")
     ap.add_argument("--no-e2e", action="store_true")

@@ -128,7 +128,7 @@ class DistributedOptimizer:
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
                  sm_budget: int | None = None, span_numel: int = 256 * 2**20,
                  param_barriers: bool = True, pre_barrier: bool | None = None,
-                 rs_push: bool | None = None):
+                 rs_push: bool | None = None, first_span_numel: int | None = None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
@@ -165,6 +165,15 @@ class DistributedOptimizer:
         # p2p/nvls: consecutive packed buckets are coalesced into one fused
         # launch until the span holds >= span_numel elements (1 = per bucket)
         self.span_numel = int(span_numel)
+        # the step's first span waits for its packs before any NVLink traffic
+        # starts: a smaller first span shortens that lead-in
+        env = os.environ.get("HOD_FIRST_SPAN")
+        if env is not None:
+            first_span_numel = int(env)
+        self.first_span_numel = (min(self.span_numel, 32 * 2**20) if first_span_numel is None
+                                 else int(first_span_numel))
+        self._spans_launched = 0
+        self._whole_step = False
         # p2p/nvls: a params-ready barrier after every span (enables per-bucket
         # wait_params for a forward-overlapped all-gather) instead of a single
         # end-of-step barrier
@@ -297,6 +306,7 @@ class DistributedOptimizer:
         self._krun = None                # open run of PDL-chained launches (timing)
         self._grads_resident = False
         self._staging = None
+        self._ev_staging_free = None
         self.step_count = 0
         self._pending_grads: list[dict[int, torch.Tensor]] = []
         self._launched: list[bool] = []
@@ -317,6 +327,7 @@ class DistributedOptimizer:
         self._launched = [False] * nb
         self._deferred_ag = []
         self._pending_span = []
+        self._spans_launched = 0
         self._deferred_pa = []
         self._ev_start.record(torch.cuda.current_stream(self.device))
         if self.clip is not None and self.backend in ("p2p", "nvls"):
@@ -376,6 +387,10 @@ class DistributedOptimizer:
         host = grads[0].device.type == "cpu"
         if host:
             self._ensure_staging(grads)
+            # the staging buffers are reused: this step's uploads must not
+            # overwrite them before the previous step's packs have read them
+            if self._ev_staging_free is not None:
+                self.s_h2d.wait_event(self._ev_staging_free)
         self.begin_step()
         if not host:
             # every gradient is already complete on the current stream: one
@@ -384,11 +399,23 @@ class DistributedOptimizer:
             # bucket k+1's ramp with bucket k's tail)
             self.s_pack.wait_stream(torch.cuda.current_stream(self.device))
             self._grads_resident = True
+        # step() returns with every bucket's params gathered (finish_step waits
+        # for all of them), so per-span params-ready barriers buy nothing
+        # here: one end-of-step barrier instead (measured d = 4: -0.06 ms)
+        self._whole_step = True
         try:
             self._step_buckets(grads, host)
+            rep = self.finish_step()
         finally:
             self._grads_resident = False
-        return self.finish_step()
+            self._whole_step = False
+        if host:
+            # every read of the staging buffers (packs, fused pack+AdamW, the
+            # post-norm pass at d = 1) runs on s_pack and is enqueued by now
+            if self._ev_staging_free is None:
+                self._ev_staging_free = torch.cuda.Event()
+            self._ev_staging_free.record(self.s_pack)
+        return rep
 
     def _step_buckets(self, grads, host: bool) -> None:
         for b in self.layout.buckets:
@@ -652,10 +679,12 @@ class DistributedOptimizer:
                 self._queue_p2p(None, final=True)
             self._pending_span.append(bi)
         pend = self._pending_span
-        full = (sum(self.layout.buckets[x].numel for x in pend) >= self.span_numel
+        target = self.first_span_numel if self._spans_launched == 0 else self.span_numel
+        full = (sum(self.layout.buckets[x].numel for x in pend) >= target
                 or len(pend) == nat.HOD_P2P_MAX_SPAN)
         if pend and (full or final):
             self._pending_span = []
+            self._spans_launched += 1
             # the pack stream is in order: the span's last pack implies the others
             self.s_comm.wait_event(self._ev_packed[pend[-1]])
             if self.clip is None:
@@ -689,7 +718,7 @@ class DistributedOptimizer:
                 self._span_done(span)
         else:
             self._queue_p2p(None, final=True)
-        if not self.param_barriers:
+        if not self.param_barriers or self._whole_step:
             # end-of-step barrier: every rank's param stores (and reads of our
             # buckets) are complete before anyone uses the params or repacks
             nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,
@@ -701,7 +730,7 @@ class DistributedOptimizer:
         """Per-span params-ready barrier: once every rank passed it, all peers'
         stores into this span's param buckets (and all reads of our grad
         buckets) are complete, so the span's params may be used / repacked."""
-        if not self.param_barriers:
+        if not self.param_barriers or self._whole_step:
             return
         nb = len(self.layout.buckets)
         nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index,

@@ -89,3 +89,25 @@ def test_padding_stays_zero_and_params_alias(native):
             pad_mask[b.start + s.offset:b.start + s.offset + s.numel] = False
     assert torch.count_nonzero(opt.grad_buffer[pad_mask]).item() == 0
     assert torch.count_nonzero(opt.param_buffer[pad_mask]).item() == 0
+
+
+@pytest.mark.parametrize("clip", [None, 1.0])
+def test_host_gradient_steps_match_resident(native, clip):
+    """step() fed from pinned HOST gradients (the e2e path: H2D into reused
+    staging buffers) equals the resident-gradient step over several steps
+    with a different gradient set each step — the uploads of step k+1 must
+    not overwrite staging that step k's packs still read."""
+    gs = config_gradset("toy")
+    p0 = init_params(gs, DEV)
+    a = DistributedOptimizer(p0, bucket_size=2_000_000, clip=clip)
+    b = DistributedOptimizer(p0, bucket_size=2_000_000, clip=clip)
+    for step in (1, 2, 3, 4):
+        grads = make_grads(gs, step, 0, DEV)
+        host = [g.cpu().pin_memory() for g in grads]
+        a.step(grads)
+        b.step(host)
+    torch.cuda.synchronize()
+    assert torch.equal(a.param_buffer, b.param_buffer)
+    assert torch.equal(a.master, b.master)
+    a.close()
+    b.close()

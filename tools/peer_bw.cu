@@ -71,3 +71,78 @@ extern "C" int peer_bw_run(const void* const* ptrs, int d, int64_t off, int64_t 
   }
   return static_cast<int>(cudaGetLastError());
 }
+
+// NVLS through the multicast address: ld_reduce (RS pattern: the switch reads
+// every copy and returns the bf16 sum), multimem.st (AG pattern: one store,
+// the switch replicates), or both per thread (the fused span kernel's mix).
+template <int VEC>
+__device__ __forceinline__ void mc_ld_reduce(const uint8_t* p, uint32_t* r) {
+  if constexpr (VEC == 16) {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "l"(p) : "memory");
+  } else {
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v2.bf16x2 {%0, %1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1]) : "l"(p) : "memory");
+  }
+}
+
+template <int VEC>
+__device__ __forceinline__ void mc_store(uint8_t* p, const uint32_t* r) {
+  if constexpr (VEC == 16) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p),
+                 "f"(__uint_as_float(r[0])), "f"(__uint_as_float(r[1])), "f"(__uint_as_float(r[2])),
+                 "f"(__uint_as_float(r[3])) : "memory");
+  } else {
+    asm volatile("multimem.st.relaxed.sys.global.v2.f32 [%0], {%1, %2};" ::"l"(p),
+                 "f"(__uint_as_float(r[0])), "f"(__uint_as_float(r[1])) : "memory");
+  }
+}
+
+// what: 1 = ld_reduce, 2 = store, 3 = both (load from off, store to off2)
+template <int VEC, int U, int WHAT>
+__global__ void __launch_bounds__(256) nvls_kernel(uint8_t* mc, int64_t off, int64_t off2, int64_t bytes,
+                                                   uint8_t* out) {
+  const int64_t n = bytes / VEC;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride * U) {
+    uint32_t r[U][4] = {};
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if ((WHAT & 1) && i + u * stride < n) mc_ld_reduce<VEC>(mc + off + (i + u * stride) * VEC, r[u]);
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (i + u * stride < n) {
+        if (WHAT & 2) mc_store<VEC>(mc + off2 + (i + u * stride) * VEC, r[u]);
+        else acc ^= r[u][0] ^ r[u][1];
+      }
+  }
+  if (acc == 0x12345678u) out[0] = 1;
+}
+
+template <int VEC, int WHAT>
+static void nvls_launch(uint8_t* mc, int64_t off, int64_t off2, int64_t bytes, uint8_t* o, int unroll, int grid,
+                        cudaStream_t s) {
+  if (unroll == 1) nvls_kernel<VEC, 1, WHAT><<<grid, 256, 0, s>>>(mc, off, off2, bytes, o);
+  else if (unroll == 2) nvls_kernel<VEC, 2, WHAT><<<grid, 256, 0, s>>>(mc, off, off2, bytes, o);
+  else nvls_kernel<VEC, 4, WHAT><<<grid, 256, 0, s>>>(mc, off, off2, bytes, o);
+}
+
+// mode 2/3/4 = nvls ld_reduce / store / both; ptr = multicast base
+extern "C" int nvls_bw_run(void* mc, int64_t off, int64_t off2, int64_t bytes, void* out, int mode, int vec,
+                           int unroll, int grid, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* m = static_cast<uint8_t*>(mc);
+  uint8_t* o = static_cast<uint8_t*>(out);
+  const int what = mode - 1;
+  if (vec == 16) {
+    if (what == 1) nvls_launch<16, 1>(m, off, off2, bytes, o, unroll, grid, s);
+    else if (what == 2) nvls_launch<16, 2>(m, off, off2, bytes, o, unroll, grid, s);
+    else nvls_launch<16, 3>(m, off, off2, bytes, o, unroll, grid, s);
+  } else {
+    if (what == 1) nvls_launch<8, 1>(m, off, off2, bytes, o, unroll, grid, s);
+    else if (what == 2) nvls_launch<8, 2>(m, off, off2, bytes, o, unroll, grid, s);
+    else nvls_launch<8, 3>(m, off, off2, bytes, o, unroll, grid, s);
+  }
+  return static_cast<int>(cudaGetLastError());
+}

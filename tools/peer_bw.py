@@ -36,6 +36,8 @@ def lib():
     L.peer_bw_run.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_int64, ctypes.c_int64,
                               ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                               ctypes.c_void_p]
+    L.nvls_bw_run.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
+                              ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
     return L
 
 
@@ -43,6 +45,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--mb", type=int, default=256)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--ops", default="read,write",
+                    help="comma list of read, write (p2p) and nvls_rs, nvls_ag, nvls_both (multicast)")
     a = ap.parse_args()
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -56,19 +60,28 @@ def main():
     nat.load()
     d = world
     chunk = a.mb << 20
-    buf = SymmetricTensor(d * chunk, torch.uint8, dev, None, zero=True)
+    ops = a.ops.split(",")
+    buf = SymmetricTensor(2 * d * chunk, torch.uint8, dev, None, zero=True)
     out = torch.zeros(16, dtype=torch.uint8, device=dev)
     ptrs = (ctypes.c_void_p * d)(*[buf.peer(q) for q in range(d)])
     s = torch.cuda.current_stream(dev)
 
+    modes = {"read": 0, "write": 1, "nvls_rs": 2, "nvls_ag": 3, "nvls_both": 4}
+
     def run(mode, vec, unroll, grid):
-        rc = L.peer_bw_run(ptrs, d, rank * chunk, chunk, out.data_ptr(), mode, vec, unroll, grid, s.cuda_stream)
+        if mode >= 2:
+            rc = L.nvls_bw_run(buf.multicast(), rank * chunk, (d + rank) * chunk, chunk, out.data_ptr(), mode, vec,
+                               unroll, grid, s.cuda_stream)
+        else:
+            rc = L.peer_bw_run(ptrs, d, rank * chunk, chunk, out.data_ptr(), mode, vec, unroll, grid,
+                               s.cuda_stream)
         assert rc == 0, rc
 
     results = []
-    for mode in (0, 1):
+    for op in ops:
+        mode = modes[op]
         for vec in (8, 16):
-            for unroll in ((1, 2, 4) if mode == 0 else (1,)):
+            for unroll in ((1, 2, 4) if mode != 1 else (1,)):
                 for grid in (148, 296, 592, 1184):
                     for _ in range(2):
                         run(mode, vec, unroll, grid)
@@ -83,9 +96,16 @@ def main():
                     t = torch.tensor([e0.elapsed_time(e1) / a.iters], device=dev)
                     dist.all_reduce(t, op=dist.ReduceOp.MAX)
                     ms = float(t)
-                    results.append({"op": "read" if mode == 0 else "write", "bytes_per_lane": vec,
-                                    "unroll": unroll, "grid": grid, "ms": round(ms, 4),
-                                    "nvlink_GBps_per_dir": round((d - 1) * chunk / ms / 1e6, 1)})
+                    r = {"op": op, "bytes_per_lane": vec, "unroll": unroll, "grid": grid, "ms": round(ms, 4),
+                         "nvlink_GBps_per_dir": round((d - 1) * chunk / ms / 1e6, 1)}
+                    if mode >= 2:
+                        # physical bytes per GPU: the switch reads every copy (rs: egress d*chunk,
+                        # ingress chunk), replicates every store (ag: egress chunk, ingress d*chunk)
+                        eg = {2: d, 3: 1, 4: d + 1}[mode] * chunk
+                        ig = {2: 1, 3: d, 4: d + 1}[mode] * chunk
+                        r.update({"egress_GBps": round(eg / ms / 1e6, 1), "ingress_GBps": round(ig / ms / 1e6, 1)})
+                        del r["nvlink_GBps_per_dir"]
+                    results.append(r)
     if rank == 0:
         for r in results:
             print(json.dumps({"world": d, "chunk_MB": a.mb, **r}))
