@@ -101,7 +101,26 @@ def main():
     ap.add_argument("--launches")
     ap.add_argument("--rep", action="append", default=[], help="name=path.ncu-rep")
     ap.add_argument("--note", default="")
+    ap.add_argument("--each", help="path.ncu-rep of tools/ncu_each.py (one launch per kernel)")
+    ap.add_argument("--each-order", help="tools/ncu_each.py stdout (launch order + algorithmic bytes)")
     a = ap.parse_args()
+    if a.each:
+        order = json.loads(Path(a.each_order).read_text().strip().splitlines()[-1])["launch_order"]
+        r = rep(Path(a.each), 1, 1, "none")["launches"]
+        if len(r) != len(order):
+            raise SystemExit(f"{len(r)} profiled launches vs {len(order)} in the launch order")
+        doc = {"round": a.round, "note": a.note, "kernels": {}}
+        for L, o in zip(r, order):
+            L.pop("elements_inferred", None)
+            tr = L["dram_read_bytes"] + L["dram_write_bytes"]
+            L.update({"elements": o.get("elems") or o.get("owned_elems"), "algorithmic_bytes": o["algorithmic_bytes"],
+                      "traffic_over_algorithmic": round(tr / o["algorithmic_bytes"], 3),
+                      "algorithmic_GBps": round(o["algorithmic_bytes"] / L["duration_us"] / 1e3, 1)})
+            doc["kernels"][o["name"]] = L
+        out = ROOT / "profiles" / f"{a.round}_ncu_each.json"
+        out.write_text(json.dumps(doc, indent=1) + "\n")
+        print(out)
+        return
     doc = {"round": a.round, "note": a.note, "kernels": {}}
     if a.launches:
         doc["launch_list"] = launches(Path(a.launches))
