@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <vector>
 
 #include "hod_common.cuh"
 
@@ -511,11 +512,20 @@ static int for_each_window(const char* who, const hod_pack_entry* entries, int n
   int64_t prev_end = 0;
   for (int i = 0; i < n_entries; ++i) {
     const hod_pack_entry& e = entries[i];
-    if (!e.src || e.numel < 0 || e.dst_offset < prev_end || e.dst_offset + e.numel > bucket_numel) {
+    // zero-element tensors (torch gives them a null data pointer) are allowed
+    if ((e.numel > 0 && !e.src) || e.numel < 0 || e.dst_offset < prev_end || e.dst_offset + e.numel > bucket_numel) {
       set_error("%s: entry %d out of order or out of bounds", who, i); return HOD_EINVAL;
     }
     prev_end = e.dst_offset + e.numel;
   }
+  // drop empty entries: they own no element (their range is padding), and a
+  // zero-length entry may share its offset with the next tensor
+  std::vector<hod_pack_entry> kept;
+  kept.reserve(n_entries);
+  for (int i = 0; i < n_entries; ++i)
+    if (entries[i].numel > 0) kept.push_back(entries[i]);
+  entries = kept.data();
+  n_entries = static_cast<int>(kept.size());
   int first = 0;
   do {
     const int cnt = (n_entries - first) < HOD_PACK_MAX_ENTRIES ? (n_entries - first) : HOD_PACK_MAX_ENTRIES;

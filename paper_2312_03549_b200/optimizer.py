@@ -131,6 +131,9 @@ class DistributedOptimizer:
                  rs_push: bool | None = None, first_span_numel: int | None = None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
+        init_params = list(init_params)
+        if not init_params:
+            raise InfeasibleConfigError("optimizer got an empty parameter list")
         self.device = (torch.device("cuda", torch.cuda.current_device()) if device is None
                        else torch.device(device))
         self.lr, self.betas, self.eps, self.weight_decay = lr, tuple(betas), eps, weight_decay
@@ -330,6 +333,12 @@ class DistributedOptimizer:
         self._spans_launched = 0
         self._deferred_pa = []
         self._ev_start.record(torch.cuda.current_stream(self.device))
+        if self.dp > 1 and self.step_count > 1:
+            # this step's packs overwrite the grad buckets the previous step's
+            # reduce-scatter read (peers included): order them after its
+            # params-ready points even if the caller skipped wait_params
+            for ev in self._ev_params:
+                self.s_pack.wait_event(ev)
         if self.clip is not None and self.backend in ("p2p", "nvls"):
             # span starts (hence the partial slots written) may differ between steps
             with torch.cuda.stream(self.s_comm):

@@ -111,3 +111,42 @@ def test_host_gradient_steps_match_resident(native, clip):
     assert torch.equal(a.master, b.master)
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("clip", [None, 0.5])
+@pytest.mark.parametrize("keep_reduced", [False, True])
+def test_ragged_and_empty_tensors_match_oracle(oracle, native, clip, keep_reduced):
+    """Zero-element, single-element and odd-sized tensors (empty slots, padding
+    tails, buckets that hold only padding) through the whole d = 1 step."""
+    shapes = [(0,), (1,), (3, 5), (0, 7), (129,), (64,), (2, 63), (1000,), (0,)]
+    g = torch.Generator(device="cpu").manual_seed(7)
+    p0 = [(torch.randn(s, generator=g) * 0.02).to(DEV) for s in shapes]
+    opt = DistributedOptimizer(p0, bucket_size=100, clip=clip, keep_reduced=keep_reduced)
+    L = opt.layout
+    state = _oracle_state(oracle, L, [p.cpu().numpy() for p in p0])
+    for step in (1, 2):
+        grads = [(torch.randn(s, generator=g) * 1e-3).to(torch.bfloat16).to(DEV) for s in shapes]
+        opt.step(grads)
+        torch.cuda.synchronize()
+        params, _ = oracle.step_all_ranks([[u16(x) for x in grads]], [
+            {"params": [(s.index, s.offset, s.numel) for s in b.slots], "numel": b.numel}
+            for b in L.buckets], state, step, opt.lr, opt.betas, opt.eps, opt.weight_decay, clip=clip)
+        pb = u16(opt.param_buffer)
+        for bi, b in enumerate(L.buckets):
+            if clip is None:
+                np.testing.assert_array_equal(pb[b.start:b.start + b.numel], params[bi])
+            else:
+                master = state[bi][0][0]
+                off = L.shard_offsets()[bi]
+                np.testing.assert_allclose(opt.master[off:off + b.numel].cpu().numpy(), master,
+                                           rtol=1e-6, atol=1e-6 * max(1e-30, np.abs(master).max()))
+    for i, p in enumerate(opt.params):
+        assert tuple(p.shape) == shapes[i]
+    opt.close()
+
+
+def test_empty_parameter_list_is_rejected(native):
+    from paper_2312_03549_b200.errors import InfeasibleConfigError
+
+    with pytest.raises(InfeasibleConfigError):
+        DistributedOptimizer([])
