@@ -420,6 +420,31 @@ def run_ours(args) -> None:
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 4 * world,
                "steps": e_steps, "path": "DistributedOptimizer.step(pinned host grads)"}
 
+    # ---- exposure inside a training iteration (N > 1) --------------------
+    # synthetic cuBLAS forward/backward of 8192 tokens per GPU around the
+    # optimizer driven as under autograd hooks (grad_ready per tensor, per-span
+    # params-ready, wait_params before each bucket's first forward use):
+    # exposed = iteration with the optimizer - iteration without (north star
+    # <= 10 %), plus SURVEY §8d's tail definition (tools/overlap_bench.py)
+    overlap = None
+    if world > 1 and not scen and not args.no_overlap:
+        if not args.no_e2e:
+            del host
+        torch.cuda.empty_cache()
+        sys.path.insert(0, str(ROOT / "tools"))
+        from overlap_bench import measure
+
+        opt.pre_barrier = True   # the hook-driven default (register_hooks)
+        o = measure(opt, gs, args.overlap_tokens, 5, world, dev)
+        overlap = {"tokens_per_gpu": args.overlap_tokens, "exposed_frac_iteration": o["iteration"]["exposed_frac"],
+                   "t_fwd_bwd_ms": o["iteration"]["t_fwd_bwd_ms"],
+                   "t_fwd_bwd_opt_ms": o["iteration"]["t_fwd_bwd_opt_ms"],
+                   "exposed_comm_frac_survey": o["exposed_comm_frac_survey"],
+                   "t_backward_ms": o["t_backward_ms"], "t_backward_with_opt_ms": o["t_overlapped_ms"],
+                   "t_optimizer_alone_ms": o["t_optimizer_alone_ms"],
+                   "note": "synthetic GEMM fwd/bwd (real cuBLAS bf16 GEMMs on the config's weight shapes); "
+                           "exposed_frac_iteration = (iter with optimizer - iter without) / iter with"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, gs, seconds=args.cpu_seconds)
@@ -439,6 +464,7 @@ def run_ours(args) -> None:
                        "l2": "inputs (~%.0f GB) >> 126 MB L2, no flush needed" % (hbm_bytes / 1e9)},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
+            "overlap": overlap,
         }
         print(json.dumps(line), flush=True)
     opt.close()
@@ -469,6 +495,8 @@ def main():
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true", help="skip the N > 1 iteration-exposure measurement")
+    ap.add_argument("--overlap-tokens", type=int, default=8192)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=30.0)
     args = ap.parse_args()

@@ -35,39 +35,10 @@ from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
 from paper_2312_03549_b200.synthetic import init_params  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--config", default="gpt1.3b")
-    ap.add_argument("--tokens", type=int, default=8192, help="micro-batch tokens per GPU (b*s)")
-    ap.add_argument("--iters", type=int, default=5)
-    ap.add_argument("--backend", default="auto")
-    ap.add_argument("--clip", type=float, default=0.0)
-    ap.add_argument("--bucket-size", type=int, default=25_000_000)
-    ap.add_argument("--sm-budget", type=int, default=0,
-                    help="CTAs per optimizer launch during backward; the backward GEMMs get the "
-                         "same number of SMs carved out (torch._C._set_sm_carveout_experimental)")
-    ap.add_argument("--pre-barrier", type=int, default=None,
-                    help="1: arrival barrier as a 1-CTA kernel before each span (optimizer pre_barrier)")
-    ap.add_argument("--rs-push", type=int, default=None, help="1: reduce-scatter by push (hod_pack_push)")
-    ap.add_argument("--span-numel", type=int, default=None, help="fused-launch span threshold (elements)")
-    a = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
-    gs = config_gradset(a.config)
-    p0 = init_params(gs, dev)
-    opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None,
-                               dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
-                               sm_budget=a.sm_budget or None,
-                               pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier),
-                               rs_push=None if a.rs_push is None else bool(a.rs_push),
-                               **({"span_numel": a.span_numel} if a.span_numel else {}))
-    del p0
-    T = a.tokens
+def measure(opt, gs, tokens: int, iters: int, world: int, dev, sm_budget: int = 0) -> dict:
+    """Backward-only and full-iteration exposure of ``opt`` with a synthetic
+    cuBLAS GEMM forward/backward of ``tokens`` tokens per GPU (see module doc)."""
+    T = tokens
     # 2-D weights get GEMMs; 1-D (norm) weights get a tiny elementwise grad
     acts = {}
     for t in gs.tensors:
@@ -130,24 +101,24 @@ def main():
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(a.iters):
+        for _ in range(iters):
             fn()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / a.iters
+        ms = e0.elapsed_time(e1) / iters
         if world > 1:
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
 
-    if a.sm_budget:
+    if sm_budget:
         # the SM carve-out is honoured by the cuBLASLt path
         torch.backends.cuda.preferred_blas_library("cublaslt")
 
     def carve(on: bool):
-        if a.sm_budget and hasattr(torch._C, "_set_sm_carveout_experimental"):
-            torch._C._set_sm_carveout_experimental(a.sm_budget if on else None)
+        if sm_budget and hasattr(torch._C, "_set_sm_carveout_experimental"):
+            torch._C._set_sm_carveout_experimental(sm_budget if on else None)
 
     def backward_carved():
         carve(True)
@@ -166,7 +137,7 @@ def main():
         opt.step(grads)
         overlapped()
     t_bwd = timed(lambda: backward(False))
-    t_bwd_carved = timed(backward_carved) if a.sm_budget else t_bwd
+    t_bwd_carved = timed(backward_carved) if sm_budget else t_bwd
     t_opt = timed(lambda: opt.step(grads))
     t_ovl = timed(overlapped)
     for _ in range(2):
@@ -201,10 +172,10 @@ def main():
     exposed = max(0.0, t_ovl - t_bwd)
     flops = sum(4 * T * t.shape[0] * t.shape[1] for t in gs.tensors if len(t.shape) == 2
                 and "embed" not in t.name)
-    doc = {"config": a.config, "world": world, "backend": opt.backend, "tokens_per_gpu": T,
+    doc = {"world": world, "backend": opt.backend, "tokens_per_gpu": T,
            "pre_barrier": opt.pre_barrier, "rs_push": opt.rs_push, "span_numel": opt.span_numel,
-           "sm_budget": a.sm_budget,
-           "clip": a.clip or None, "buckets": len(opt.layout.buckets), "bucket_size": a.bucket_size,
+           "sm_budget": sm_budget,
+           "clip": opt.clip, "buckets": len(opt.layout.buckets),
            "t_backward_ms": round(t_bwd, 3), "t_backward_carved_ms": round(t_bwd_carved, 3),
            "t_optimizer_alone_ms": round(t_opt, 3),
            "timeline": {"backward_end_ms": round(bwd_end_ms, 3), "first_opt_kernel_start_ms": round(first_start, 3),
@@ -222,6 +193,43 @@ def main():
                                              / max((e for _, _, e in spans), default=1.0), 4),
            "hidden_frac_of_optimizer": round(1 - exposed / t_opt, 4) if t_opt > 0 else None,
            "backward_tflops": round(flops / (t_bwd / 1e3) / 1e12, 1)}
+    return doc
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="gpt1.3b")
+    ap.add_argument("--tokens", type=int, default=8192, help="micro-batch tokens per GPU (b*s)")
+    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--backend", default="auto")
+    ap.add_argument("--clip", type=float, default=0.0)
+    ap.add_argument("--bucket-size", type=int, default=25_000_000)
+    ap.add_argument("--sm-budget", type=int, default=0,
+                    help="CTAs per optimizer launch during backward; the backward GEMMs get the "
+                         "same number of SMs carved out (torch._C._set_sm_carveout_experimental)")
+    ap.add_argument("--pre-barrier", type=int, default=None,
+                    help="1: arrival barrier as a 1-CTA kernel before each span (optimizer pre_barrier)")
+    ap.add_argument("--rs-push", type=int, default=None, help="1: reduce-scatter by push (hod_pack_push)")
+    ap.add_argument("--span-numel", type=int, default=None, help="fused-launch span threshold (elements)")
+    a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    gs = config_gradset(a.config)
+    p0 = init_params(gs, dev)
+    opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None,
+                               dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
+                               sm_budget=a.sm_budget or None,
+                               pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier),
+                               rs_push=None if a.rs_push is None else bool(a.rs_push),
+                               **({"span_numel": a.span_numel} if a.span_numel else {}))
+    del p0
+    doc = measure(opt, gs, a.tokens, a.iters, world, dev, sm_budget=a.sm_budget)
+    doc.update({"config": a.config, "bucket_size": a.bucket_size})
     if rank == 0:
         print(json.dumps(doc))
     if world > 1:
