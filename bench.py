@@ -245,6 +245,65 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def north_star_probe(args, world: int, rank: int, dev) -> dict:
+    """BASELINE.json's target workload measured inside the default run at
+    N >= 4: the LLaMA-7B real tensor list, bf16 grads, clip 1.0, DP = N —
+    standalone step time (CUDA events, max over ranks) and the exposure of
+    the optimizer inside a training iteration (synthetic cuBLAS fwd/bwd of
+    ``--overlap-tokens`` tokens per GPU, tools/overlap_bench.py)."""
+    import torch
+
+    from paper_2312_03549_b200 import DistributedOptimizer
+    from paper_2312_03549_b200.comm import DPGroup
+    from paper_2312_03549_b200.gradsets import config_gradset
+    from paper_2312_03549_b200.synthetic import init_params, make_grads
+
+    gs = config_gradset("llama7b")
+    p0 = init_params(gs, dev)
+    opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=1.0,
+                               dp_group=DPGroup(tuple(range(world)), rank), span_numel=args.span_numel)
+    del p0
+    torch.cuda.empty_cache()
+    grads = make_grads(gs, 1, rank, dev)
+    for _ in range(3):
+        opt.step(grads)
+    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 5
+    e0.record()
+    for _ in range(steps):
+        opt.step(grads)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    del grads
+    torch.cuda.empty_cache()
+    sys.path.insert(0, str(ROOT / "tools"))
+    from overlap_bench import measure
+
+    opt.pre_barrier = True   # the hook-driven default (register_hooks)
+    o = measure(opt, gs, args.overlap_tokens, 3, world, dev)
+    P, d = gs.total, world
+    peak, _ = _peaks()
+    hbm = 4 * P + 30 * P / d                  # pack + AdamW 28 B + norm read 2 B per owned element
+    nvl = 4 * P * (d - 1) / d
+    t_roof = max(hbm / (peak * 1e9), nvl / (NVLINK_MEASURED * 1e9)) * 1e3
+    out = {"workload": f"LLaMA-7B real tensor list, bf16 grads, grad-norm clip 1.0, DP={world} "
+                       f"(BASELINE.json target; backend {opt.backend})",
+           "params": gs.total, "ms_per_step": ms, "params_per_s": gs.total / (ms / 1e3), "steps": steps,
+           "step_roofline": {"t_roof_ms": t_roof, "frac": t_roof / ms,
+                             "bound": "hbm" if hbm / (peak * 1e9) >= nvl / (NVLINK_MEASURED * 1e9) else "nvlink"},
+           "overlap": {"tokens_per_gpu": args.overlap_tokens,
+                       "exposed_frac_iteration": o["iteration"]["exposed_frac"],
+                       "t_fwd_bwd_ms": o["iteration"]["t_fwd_bwd_ms"],
+                       "t_fwd_bwd_opt_ms": o["iteration"]["t_fwd_bwd_opt_ms"],
+                       "exposed_comm_frac_survey": o["exposed_comm_frac_survey"],
+                       "t_optimizer_alone_ms": o["t_optimizer_alone_ms"]}}
+    opt.close()
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args) -> None:
     import torch
 
@@ -445,6 +504,14 @@ def run_ours(args) -> None:
                    "note": "synthetic GEMM fwd/bwd (real cuBLAS bf16 GEMMs on the config's weight shapes); "
                            "exposed_frac_iteration = (iter with optimizer - iter without) / iter with"}
 
+    opt_info = {"buckets": len(opt.layout.buckets), "dp": opt.dp, "backend": opt.backend}
+    ns = None
+    if args.north_star == 1 or (args.north_star == -1 and world >= 4 and not scen and args.config == "gpt1.3b"):
+        opt.close()
+        opt = None
+        torch.cuda.empty_cache()
+        ns = north_star_probe(args, world, rank, dev)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, gs, seconds=args.cpu_seconds)
@@ -459,15 +526,16 @@ def run_ours(args) -> None:
                                     if scen else _desc(cfg, clip)),
                        "config": "scenario" if scen else args.config, "params": params_per_step,
                        "scenario": scen,
-                       "buckets": len(opt.layout.buckets), "bucket_size": args.bucket_size,
-                       "dp": opt.dp, "clip": clip, "backend": opt.backend,
+                       "buckets": opt_info["buckets"], "bucket_size": args.bucket_size,
+                       "dp": opt_info["dp"], "clip": clip, "backend": opt_info["backend"],
                        "l2": "inputs (~%.0f GB) >> 126 MB L2, no flush needed" % (hbm_bytes / 1e9)},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
-            "overlap": overlap,
+            "overlap": overlap, "north_star_llama7b": ns,
         }
         print(json.dumps(line), flush=True)
-    opt.close()
+    if opt is not None:
+        opt.close()
     if world > 1:
         import torch.distributed as dist
 
@@ -497,6 +565,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="skip the N > 1 iteration-exposure measurement")
     ap.add_argument("--overlap-tokens", type=int, default=8192)
+    ap.add_argument("--north-star", type=int, default=-1, choices=[-1, 0, 1],
+                    help="also measure the LLaMA-7B clip DP=N target (step + iteration exposure); "
+                         "-1 = on for the default config at N >= 4")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=30.0)
     args = ap.parse_args()
