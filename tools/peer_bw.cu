@@ -49,6 +49,32 @@ __global__ void __launch_bounds__(256) peer_write(Peers ps, int d, int64_t off, 
       if (q < d) reinterpret_cast<V*>(const_cast<uint8_t*>(ps.p[q]) + off)[i] = z;
 }
 
+// both: each thread pulls VEC bytes of its shard from every peer (RS) and
+// stores VEC bytes to every peer's second region (AG) — the fused p2p mix
+template <int VEC>
+__global__ void __launch_bounds__(256) peer_both(Peers ps, int d, int64_t off, int64_t off2, int64_t bytes,
+                                                 uint8_t* out) {
+  using V = typename std::conditional<VEC == 16, uint4, uint2>::type;
+  const int64_t n = bytes / VEC;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  uint32_t acc = 0;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    V v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < d) v[q] = reinterpret_cast<const V*>(ps.p[q] + off)[i];
+    V s = v[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < d) s.x ^= v[q].x;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q < d) reinterpret_cast<V*>(const_cast<uint8_t*>(ps.p[q]) + off2)[i] = s;
+    acc ^= s.y;
+  }
+  if (acc == 0x12345678u) out[0] = 1;
+}
+
 extern "C" int peer_bw_run(const void* const* ptrs, int d, int64_t off, int64_t bytes, void* out, int mode,
                            int vec, int unroll, int grid, void* stream) {
   Peers ps{};
@@ -65,9 +91,13 @@ extern "C" int peer_bw_run(const void* const* ptrs, int d, int64_t off, int64_t 
       else if (unroll == 2) peer_read<8, 2><<<grid, 256, 0, s>>>(ps, d, off, bytes, o);
       else peer_read<8, 4><<<grid, 256, 0, s>>>(ps, d, off, bytes, o);
     }
-  } else {
+  } else if (mode == 1) {
     if (vec == 16) peer_write<16><<<grid, 256, 0, s>>>(ps, d, off, bytes);
     else peer_write<8><<<grid, 256, 0, s>>>(ps, d, off, bytes);
+  } else {
+    // mode 5: both (second region at off + d * bytes)
+    if (vec == 16) peer_both<16><<<grid, 256, 0, s>>>(ps, d, off, off + d * bytes, bytes, o);
+    else peer_both<8><<<grid, 256, 0, s>>>(ps, d, off, off + d * bytes, bytes, o);
   }
   return static_cast<int>(cudaGetLastError());
 }

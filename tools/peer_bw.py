@@ -46,7 +46,7 @@ def main():
     ap.add_argument("--mb", type=int, default=256)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--ops", default="read,write",
-                    help="comma list of read, write (p2p) and nvls_rs, nvls_ag, nvls_both (multicast)")
+                    help="comma list of read, write, both (p2p) and nvls_rs, nvls_ag, nvls_both (multicast)")
     a = ap.parse_args()
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -66,10 +66,10 @@ def main():
     ptrs = (ctypes.c_void_p * d)(*[buf.peer(q) for q in range(d)])
     s = torch.cuda.current_stream(dev)
 
-    modes = {"read": 0, "write": 1, "nvls_rs": 2, "nvls_ag": 3, "nvls_both": 4}
+    modes = {"read": 0, "write": 1, "nvls_rs": 2, "nvls_ag": 3, "nvls_both": 4, "both": 5}
 
     def run(mode, vec, unroll, grid):
-        if mode >= 2:
+        if mode in (2, 3, 4):
             rc = L.nvls_bw_run(buf.multicast(), rank * chunk, (d + rank) * chunk, chunk, out.data_ptr(), mode, vec,
                                unroll, grid, s.cuda_stream)
         else:
@@ -81,7 +81,7 @@ def main():
     for op in ops:
         mode = modes[op]
         for vec in (8, 16):
-            for unroll in ((1, 2, 4) if mode != 1 else (1,)):
+            for unroll in ((1, 2, 4) if mode not in (1, 5) else (1,)):
                 for grid in (148, 296, 592, 1184):
                     for _ in range(2):
                         run(mode, vec, unroll, grid)
@@ -98,7 +98,10 @@ def main():
                     ms = float(t)
                     r = {"op": op, "bytes_per_lane": vec, "unroll": unroll, "grid": grid, "ms": round(ms, 4),
                          "nvlink_GBps_per_dir": round((d - 1) * chunk / ms / 1e6, 1)}
-                    if mode >= 2:
+                    if mode == 5:
+                        # RS in + AG in from the peers' stores, per direction
+                        r["nvlink_GBps_per_dir"] = round(2 * (d - 1) * chunk / ms / 1e6, 1)
+                    if mode in (2, 3, 4):
                         # physical bytes per GPU: the switch reads every copy (rs: egress d*chunk,
                         # ingress chunk), replicates every store (ag: egress chunk, ingress d*chunk)
                         eg = {2: d, 3: 1, 4: d + 1}[mode] * chunk
