@@ -304,6 +304,86 @@ def north_star_probe(args, world: int, rank: int, dev) -> dict:
     return out
 
 
+def scenario_probe(args, path: Path, world: int, rank: int, dev) -> dict:
+    """BASELINE config 4 inside the default run: the reference planner's
+    self-adapting partition and DP rows for ``path`` (PP x DP over the world),
+    every stage's DP row running its own optimizer, world clip norm; step time
+    = max over ranks (CUDA events)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2312_03549_b200 as hp
+    from paper_2312_03549_b200.scenario_run import make_optimizer, setup_rank
+    from paper_2312_03549_b200.synthetic import init_params, make_grads
+
+    scenario = hp.load_scenario(str(path))
+    sr = setup_rank(scenario, rank)
+    gs = sr.gradset
+    p0 = init_params(gs, dev)
+    opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=1.0, span_numel=args.span_numel)
+    del p0
+    torch.cuda.empty_cache()
+    grads = make_grads(gs, 1, rank, dev)
+    for _ in range(3):
+        opt.step(grads)
+    _barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 5
+    e0.record()
+    for _ in range(steps):
+        opt.step(grads)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, {sr.placement.stage: gs.total})
+    totals = {}
+    for dct in gathered:
+        totals.update(dct)
+    out = {"scenario": path.name, "stage_layers": list(hp.partition_scenario(scenario).stage_layers),
+           "stage_params": totals, "dp_ranks_rank0": list(sr.placement.dp_ranks), "backend": opt.backend,
+           "ms_per_step": ms, "params_per_s": sum(totals.values()) / (ms / 1e3), "steps": steps}
+    opt.close()
+    del grads, opt
+    torch.cuda.empty_cache()
+    return out
+
+
+def sweep_probe(world: int, rank: int, dev) -> list:
+    """BASELINE config 5 inside the default run: one bucket of 1 MB .. 1 GB,
+    fused RS+AdamW+AG (p2p, nvls) vs NCCL ReduceScatter+AllGather, busBW
+    (tools/p2p_microbench.py)."""
+    import torch
+
+    from paper_2312_03549_b200.comm import NcclComm
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    from p2p_microbench import measure_bucket
+
+    comm = NcclComm(tuple(range(world)), rank, "sweep")
+    rows = []
+    for numel in (1 << 19, 1 << 23, 1 << 26, 1 << 29):     # 1 MB, 16 MB, 128 MB, 1 GB of bf16
+        iters = max(5, min(50, int(2e9 // (numel * 2))))
+        doc = measure_bucket(numel, iters, world, rank, dev, comm,
+                             cases=("fused_p2p", "fused_nvls", "nccl_rs+ag"))
+        rows.append({"bucket_MB": doc["bucket_MB"],
+                     **{k: {"ms": v["ms"], "busBW_GBps": v["busBW_GBps"]} for k, v in doc["results"].items()
+                        if isinstance(v, dict)}})
+    comm.close()
+    torch.cuda.empty_cache()
+    return rows
+
+
+def _guarded(name, fn, world):
+    """Run one add-on probe; a failure is recorded in the line, not fatal."""
+    try:
+        out = fn()
+    except Exception as e:  # noqa: BLE001  (the main measurement must still print)
+        out = {"error": f"{type(e).__name__}: {e}"[:300]}
+    _barrier(world)
+    return out
+
+
 def run_ours(args) -> None:
     import torch
 
@@ -505,12 +585,20 @@ def run_ours(args) -> None:
                            "exposed_frac_iteration = (iter with optimizer - iter without) / iter with"}
 
     opt_info = {"buckets": len(opt.layout.buckets), "dp": opt.dp, "backend": opt.backend}
-    ns = None
-    if args.north_star == 1 or (args.north_star == -1 and world >= 4 and not scen and args.config == "gpt1.3b"):
+    extras = None
+    if args.extras == 1 or (args.extras == -1 and world >= 4 and not scen and args.config == "gpt1.3b"):
+        # the driver's multi-GPU runs use the default config: measure the other
+        # BASELINE configs at this N too (config 3 target, config 4, config 5)
         opt.close()
         opt = None
         torch.cuda.empty_cache()
-        ns = north_star_probe(args, world, rank, dev)
+        scen_file = ROOT / "scenarios" / ("gpt13b_pp2_dp4_hybrid.json" if world == 8 else
+                                          "gpt13b_pp2_dp2_hybrid.json")
+        extras = {"north_star_llama7b": _guarded("llama", lambda: north_star_probe(args, world, rank, dev), world)}
+        if world in (4, 8):
+            extras["config4_scenario"] = _guarded("scenario", lambda: scenario_probe(args, scen_file, world, rank,
+                                                                                      dev), world)
+        extras["config5_sweep"] = _guarded("sweep", lambda: sweep_probe(world, rank, dev), world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -531,7 +619,7 @@ def run_ours(args) -> None:
                        "l2": "inputs (~%.0f GB) >> 126 MB L2, no flush needed" % (hbm_bytes / 1e9)},
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
-            "overlap": overlap, "north_star_llama7b": ns,
+            "overlap": overlap, "extras": extras,
         }
         print(json.dumps(line), flush=True)
     if opt is not None:
@@ -565,8 +653,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="skip the N > 1 iteration-exposure measurement")
     ap.add_argument("--overlap-tokens", type=int, default=8192)
-    ap.add_argument("--north-star", type=int, default=-1, choices=[-1, 0, 1],
-                    help="also measure the LLaMA-7B clip DP=N target (step + iteration exposure); "
+    ap.add_argument("--extras", type=int, default=-1, choices=[-1, 0, 1],
+                    help="also measure BASELINE configs 3 (LLaMA-7B clip DP=N: step + iteration exposure), "
+                         "4 (13B PP=2 x DP=N/2 scenario) and 5 (bucket sweep) at this N; "
                          "-1 = on for the default config at N >= 4")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--ref-seconds", type=float, default=30.0)

@@ -28,36 +28,33 @@ from paper_2312_03549_b200.symm import SymmetricTensor  # noqa: E402
 
 
 def main():
-    import argparse as _ap
-
-    pre = _ap.ArgumentParser(add_help=False)
-    pre.add_argument("--sweep", action="store_true")
-    known, _ = pre.parse_known_args()
-    if known.sweep:
-        sizes = [(1 << 20) // 2 * (1 << k) for k in range(11)]      # 0.5M .. 512M elements
-        for n in sizes:
-            run_one(n, sweep=True)
-        return
-    run_one(None)
-
-
-def run_one(numel_override, sweep=False):
     ap = argparse.ArgumentParser()
     ap.add_argument("--numel", type=int, default=104_857_600)
     ap.add_argument("--sweep", action="store_true",
                     help="BASELINE config 5: bucket sizes 1 MB .. 1 GB (0.5M .. 512M bf16 elements)")
     ap.add_argument("--iters", type=int, default=20)
-    a, _ = ap.parse_known_args()
-    if numel_override is not None:
-        a.numel = numel_override
-        a.iters = max(5, min(50, int(2e9 // (a.numel * 2))))
+    a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(rank)
-    if not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", rank))
-    dev = torch.device("cuda", rank)
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
     nat.load()
-    N = a.numel - a.numel % (16 * world)
+    comm = NcclComm(tuple(range(world)), rank, "bench")
+    sizes = [(1 << 20) // 2 * (1 << k) for k in range(11)] if a.sweep else [a.numel]
+    for numel in sizes:
+        iters = max(5, min(50, int(2e9 // (numel * 2)))) if a.sweep else a.iters
+        doc = measure_bucket(numel, iters, world, rank, dev, comm)
+        if rank == 0:
+            print(json.dumps(doc, indent=None if a.sweep else 1), flush=True)
+    comm.close()
+    dist.destroy_process_group()
+
+
+def measure_bucket(numel, iters, world, rank, dev, comm, cases=None) -> dict:
+    """Time the fused kernels and NCCL RS+AG on one bucket of ``numel`` bf16
+    elements (CUDA events, max over ranks); ``cases`` limits the set."""
+    N = numel - numel % (16 * world)
     n = N // world
     pg = dist.group.WORLD
     g = SymmetricTensor(N, torch.bfloat16, dev, pg)
@@ -105,8 +102,6 @@ def run_one(numel_override, sweep=False):
             sp.clip_coef = coef.data_ptr()
         nat.call("hod_p2p_step", ctypes.byref(sp), mode, ctypes.byref(hp), s.cuda_stream)
 
-    comm = NcclComm(tuple(range(world)), rank, "bench")
-
     def nccl_rs_ag():
         base = g.tensor.data_ptr()
         comm.reduce_scatter_bf16(base, base + 2 * rank * n, n, s)
@@ -116,7 +111,7 @@ def run_one(numel_override, sweep=False):
         nat.call("hod_adamw_bf16", master.data_ptr(), m.data_ptr(), v.data_ptr(), red.data_ptr(),
                  p.tensor.data_ptr() + 2 * rank * n, n, ctypes.byref(hp), None, s.cuda_stream)
 
-    cases = {
+    all_cases = {
         "fused_p2p": lambda: run_mode(nat.HOD_P2P_FUSED, False),
         "rs_p2p": lambda: run_mode(nat.HOD_P2P_RS, False),
         "adamw_ag_p2p": lambda: run_mode(nat.HOD_P2P_ADAMW_AG, False),
@@ -127,18 +122,20 @@ def run_one(numel_override, sweep=False):
         "adamw_local": adamw_local,
     }
     out = {}
-    for name, fn in cases.items():
+    for name, fn in all_cases.items():
+        if (cases is not None and name not in cases) or ("nvls" in name and not (g.mc and p.mc)):
+            continue
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
         dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(a.iters):
+        for _ in range(iters):
             fn()
         e1.record()
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1) / a.iters], device=dev, dtype=torch.float64)
+        t = torch.tensor([e0.elapsed_time(e1) / iters], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         nvl = 4 * n * (world - 1) if "fused" in name or "nccl" in name else 2 * n * (world - 1)
@@ -152,14 +149,10 @@ def run_one(numel_override, sweep=False):
                      "busBW_GBps": round(bus, 1) if bus else None}
     if int(err.item()):
         out["error"] = int(err.item())
-    if rank == 0:
-        print(json.dumps({"world": world, "numel": N, "bucket_MB": round(2 * N / 2**20, 2), "shard": n,
-                          "results": out}, indent=None if sweep else 1), flush=True)
-    comm.close()
+    doc = {"world": world, "numel": N, "bucket_MB": round(2 * N / 2**20, 2), "shard": n, "results": out}
     del g, p, fl
     torch.cuda.empty_cache()
-    if not sweep:
-        dist.destroy_process_group()
+    return doc
 
 
 if __name__ == "__main__":
