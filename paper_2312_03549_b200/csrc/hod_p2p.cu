@@ -157,11 +157,19 @@ __device__ __forceinline__ void st_multicast8(uint16_t* mc, const uint2& q) {
 // Quads never straddle buckets (shards are multiples of 16 elements); each
 // quad is located on its own.  Split into a load phase and a compute/store
 // phase so U items can have all their loads in flight at once.
-template <int D, int kSrc>
+template <int D, int kSrc, int W = 0>
 struct Item {
   static constexpr int kRaw = kSrc == kSrcNvls ? 1 : (D > 0 ? D : kMaxRanks);
+  // W (wide, p2p pull only): the peers' bucket vectors are pulled 16 bytes
+  // per lane (8 contiguous elements, half the load instructions of two 8-byte
+  // quads; measured d = 2 read+write ceiling 678 vs 641 GB/s), reduced, and
+  // the reduced bf16 quads are shuffled to the quad-pair mapping of the state
+  static constexpr bool kWide = W != 0 && kSrc == kSrcPeer;
   uint2 raw[2][kRaw];  // per quad: peers' bucket vectors (p2p), the switch-reduced
                        // vector (nvls) or the local reduced shard (mode 2, raw[h][0])
+  uint4 raw8[kWide ? kRaw : 1];  // wide: the peers' 8-element vectors at e8
+  int64_t e8;          // wide: element offset of this lane's 8 contiguous elements
+  bool ok8;
   float4 st[2][3];     // per quad: master, m, v
   int64_t e[2];        // element offset in the flat buffers
   int64_t s[2];        // element offset in the span's state
@@ -178,6 +186,7 @@ template <typename ItemT>
 __device__ __forceinline__ void locate_chunk(const SpanArgs& a, int64_t ch, int lane, int& k, ItemT& it) {
   if (ch >= a.chunk_end[a.n_buckets - 1]) {
     it.ok[0] = it.ok[1] = false;
+    it.ok8 = false;
     return;
   }
   while (k < a.n_buckets - 1 && ch >= a.chunk_end[k]) ++k;
@@ -186,6 +195,8 @@ __device__ __forceinline__ void locate_chunk(const SpanArgs& a, int64_t ch, int 
   const int64_t n = a.shard_n[k];
   const int64_t own = a.own_off[k];
   const int64_t base = (ch - first_chunk) * kChunk + lane * 4;
+  it.e8 = own + (ch - first_chunk) * kChunk + lane * 8;
+  it.ok8 = (ch - first_chunk) * kChunk + lane * 8 < n;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const int64_t off = base + h * 128;
@@ -196,8 +207,17 @@ __device__ __forceinline__ void locate_chunk(const SpanArgs& a, int64_t ch, int 
   }
 }
 
-template <int D, int kSrc, int kMode>
-__device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kSrc>& it, int rank) {
+template <int D, int kSrc, int kMode, int W>
+__device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kSrc, W>& it, int rank) {
+  using ItemT = Item<D, kSrc, W>;
+  if constexpr (ItemT::kWide && kMode != 2) {
+    if (it.ok8) {
+      const int dd = D > 0 ? D : a.d;
+#pragma unroll
+      for (int q = 0; q < ItemT::kRaw; ++q)
+        if (q < dd) it.raw8[q] = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + it.e8);
+    }
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (!it.ok[h]) continue;
@@ -211,12 +231,12 @@ __device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kSrc>& it, 
       const int dd = D > 0 ? D : a.d;
       const uint16_t* base = a.local_grad + e - static_cast<int64_t>(rank) * it.sn[h];
 #pragma unroll
-      for (int q = 0; q < Item<D, kSrc>::kRaw; ++q)
+      for (int q = 0; q < ItemT::kRaw; ++q)
         if (q < dd) it.raw[h][q] = *reinterpret_cast<const uint2*>(base + q * it.sn[h]);
-    } else {
+    } else if constexpr (!ItemT::kWide) {
       const int dd = D > 0 ? D : a.d;
 #pragma unroll
-      for (int q = 0; q < Item<D, kSrc>::kRaw; ++q)
+      for (int q = 0; q < ItemT::kRaw; ++q)
         if (q < dd) it.raw[h][q] = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(a.grad.p[q]) + e);
     }
     if (kMode != 1) {
@@ -239,20 +259,54 @@ __device__ __forceinline__ void gather_store4(const SpanArgs& a, int64_t e, cons
   }
 }
 
-template <int D, int kSrc, int kMode>
-__device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSrc>& it,
+template <int D, int kSrc, int kMode, int W>
+__device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSrc, W>& it,
                                             const AdamWConsts& c, float coef, float& ss) {
+  using ItemT = Item<D, kSrc, W>;
+  uint2 red[2];
+  if constexpr (ItemT::kWide && kMode != 2) {
+    // reduce this lane's 8 contiguous elements over the d peers (rank order,
+    // fp32, one RNE rounding: the same per-element arithmetic as the quad
+    // path), then lane l takes quad l from lane l/2 and quad 32+l from lane
+    // 16+l/2 (half l&1 of the source's 8 elements).  Whole warp participates.
+    uint4 r8 = make_uint4(0u, 0u, 0u, 0u);
+    if (it.ok8) {
+      const int dd = D > 0 ? D : a.d;
+      float acc[8] = {0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int q = 0; q < ItemT::kRaw; ++q) {
+        if (q < dd) {
+          float f[8];
+          unpack8(it.raw8[q], f);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
+        }
+      }
+      r8 = pack8(acc);
+    }
+    const int lane = threadIdx.x & 31;
+    const bool hi = lane & 1;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int src = h * 16 + (lane >> 1);
+      const uint32_t x = __shfl_sync(0xffffffffu, r8.x, src), y = __shfl_sync(0xffffffffu, r8.y, src);
+      const uint32_t z = __shfl_sync(0xffffffffu, r8.z, src), w = __shfl_sync(0xffffffffu, r8.w, src);
+      red[h] = hi ? make_uint2(z, w) : make_uint2(x, y);
+    }
+  }
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     if (!it.ok[h]) continue;
     float g[4];
     if (kMode == 2 || kSrc == kSrcNvls) {
       unpack4(it.raw[h][0], g);
+    } else if constexpr (ItemT::kWide) {
+      unpack4(red[h], g);
     } else {
       const int dd = D > 0 ? D : a.d;
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int q = 0; q < Item<D, kSrc>::kRaw; ++q) {
+      for (int q = 0; q < ItemT::kRaw; ++q) {
         if (q < dd) {
           float f[4];
           unpack4(it.raw[h][q], f);
@@ -290,7 +344,7 @@ __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSr
 // kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+in-place reduced shard, partials),
 // 2 = AdamW+AG from the in-place reduced shard.  U: items per thread in flight
 // (memory-level parallelism for the NVLink loads).
-template <int D, int kSrc, int kMode, int U>
+template <int D, int kSrc, int kMode, int U, int W>
 __global__ void __launch_bounds__(kThreads, HOD_P2P_MINB) p2p_step_kernel(const __grid_constant__ SpanArgs a,
                                                              const BarrierArgs b, const AdamWConsts c,
                                                              int rank) {
@@ -307,15 +361,15 @@ __global__ void __launch_bounds__(kThreads, HOD_P2P_MINB) p2p_step_kernel(const 
   for (int u = 0; u < U; ++u) cur[u] = 0;
   for (int64_t base = (static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x) >> 5; base < n_chunks;
        base += n_warps * U) {
-    Item<D, kSrc> it[U];
+    Item<D, kSrc, W> it[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t ch = base + u * n_warps;
       locate_chunk(a, ch, lane, cur[u], it[u]);
-      load_item<D, kSrc, kMode>(a, it[u], rank);
+      load_item<D, kSrc, kMode, W>(a, it[u], rank);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) finish_item<D, kSrc, kMode>(a, it[u], c, coef, ss);
+    for (int u = 0; u < U; ++u) finish_item<D, kSrc, kMode, W>(a, it[u], c, coef, ss);
   }
   if (kMode == 1 && a.partials) {
     const float s = block_sum_f(ss);
@@ -388,6 +442,18 @@ static int unroll_setting() {
   return u;
 }
 
+// 16-byte peer loads in the p2p pull reduce-scatter (Item::kWide): default
+// on at d = 2 (measured: fused span kernel -2.3 %, LLaMA-7B RS -1 %; the
+// d = 4 read ceiling is the same for 8- and 16-byte loads); env
+// HOD_P2P_WIDE=0/1 forces it off/on
+static int wide_setting() {
+  static int w = [] {
+    const char* e = getenv("HOD_P2P_WIDE");
+    return e ? atoi(e) : -1;
+  }();
+  return w;
+}
+
 template <int D, int kSrc, int kMode>
 static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWConsts& c, int rank,
                         int grid, cudaStream_t s) {
@@ -395,10 +461,15 @@ static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWCons
   // measured (tools/p2p_microbench.py): two items in flight per thread pay off
   // at d = 2 (one remote load each); at d >= 4 the register cost outweighs it
   const int u = unroll_setting();
-  if (u >= 2 || (u == 0 && D == 2))
-    p2p_step_kernel<D, kSrc, kMode, 2><<<grid, kThreads, 0, s>>>(a, b, c, rank);
-  else
-    p2p_step_kernel<D, kSrc, kMode, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+  const bool two = u >= 2 || (u == 0 && D == 2);
+  const int w = wide_setting();
+  if (kSrc == kSrcPeer && kMode != 2 && (w > 0 || (w < 0 && D == 2))) {
+    if (two) p2p_step_kernel<D, kSrc, kMode, 2, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+    else p2p_step_kernel<D, kSrc, kMode, 1, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+  } else {
+    if (two) p2p_step_kernel<D, kSrc, kMode, 2, 0><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+    else p2p_step_kernel<D, kSrc, kMode, 1, 0><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+  }
 }
 
 template <int kSrc, int kMode>
