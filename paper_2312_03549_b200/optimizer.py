@@ -17,12 +17,15 @@ plus all-gather of the stage's gradient bytes charged after the pipeline
 flush (simulator.py:327-333, 445-452) — with the real,
 overlapped operation.  The ``backend`` selects how C1/C2 move bytes:
 
-* ``"p2p"`` (default for d > 1) — our fused kernels over NVLink peer memory:
-  one kernel per bucket does the cross-GPU arrival barrier, the
-  reduce-scatter (P2P loads, fp32 rank-order sum: deterministic and bit-exact
-  with the oracle), the AdamW update and the all-gather (P2P stores).
-* ``"nvls"`` — the same fused kernel with NVSwitch in-switch reduction
-  (multimem.ld_reduce) and multicast stores (multimem.st).
+* ``"p2p"`` (``"auto"`` at d = 2, and at any d with clipping) — our fused
+  kernels over NVLink peer memory: one kernel per span of consecutive packed
+  buckets does the cross-GPU arrival barrier, the reduce-scatter (P2P loads,
+  fp32 rank-order sum: deterministic and bit-exact with the oracle), the
+  AdamW update and the all-gather (P2P stores); with clipping the RS and the
+  AdamW+AG halves run as two kernels around the peer-memory norm exchange.
+* ``"nvls"`` (``"auto"`` from d = 4 without clipping) — the same fused kernel
+  with NVSwitch in-switch reduction (multimem.ld_reduce) and multicast
+  stores (multimem.st).
 * ``"nccl"`` — NCCL ReduceScatter / AllGather (bf16, sum) around our K2; the
   library baseline the fused path is measured against.
 * ``"none"`` — d == 1: no collective, AdamW reads the packed bucket.
