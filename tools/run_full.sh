@@ -22,7 +22,7 @@ if [ $N -ge 4 ]; then
     > $O/${TAG}_bench_gpt13b_pp2dp2_n4.log 2>&1
 fi
 timeout 600 python bench.py --impl reference > $O/${TAG}_bench_reference_n1.log 2>&1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv \
   --log-file $O/${TAG}_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline \
   > $O/${TAG}_ncu_launches.log 2>&1
 grep -h '"metric"' $O/${TAG}_bench_*.log | cut -c1-160
