@@ -181,6 +181,24 @@ def _traffic_from_profile(kernel: str):
     return None, None, None
 
 
+def _emulated_traffic_ratio(dom: str, d: int, backend: str):
+    """DRAM traffic / algorithmic bytes of the span kernel from the one-GPU
+    emulated ncu capture (profiles/*_ncu_each.json, tools/ncu_each.py): a
+    multi-rank kernel cannot be replayed under ncu, its peers' copies are
+    local there.  p2p only (multicast has no single-GPU stand-in)."""
+    if backend != "p2p":
+        return None
+    for p in sorted((ROOT / "profiles").glob("*ncu_each.json"), reverse=True):
+        try:
+            k = json.loads(p.read_text())["kernels"].get(f"span_{dom}_d{d}")
+        except Exception:
+            continue
+        if k and k.get("traffic_over_algorithmic"):
+            return {"traffic_over_algorithmic": k["traffic_over_algorithmic"], "source": f"{p.name}:span_{dom}_d{d}",
+                    "note": "one-GPU emulation of the d-way kernel (peer copies local), cold cache"}
+    return None
+
+
 def cpu_baseline(config: str, gs, seconds: float = 10.0) -> dict:
     """Oracle (CPU port) timed on a bounded sample: pack + AdamW over whole
     buckets of the workload, repeated until ``seconds`` elapse."""
@@ -498,6 +516,7 @@ def run_ours(args) -> None:
             phys = {"fused": 2 * (d_ + 1), "adamw_ag": 2 * d_, "rs": 2 * d_}[dom]
             nvl_view["physical_bytes_per_owned_element"] = phys
             nvl_view["physical_achieved"] = elems * phys / (ktime / 1e3) / 1e9 if ktime > 0 else None
+        roof["traffic_emulated"] = _emulated_traffic_ratio(dom, d_, opt.backend)
         if hbm_elem / peak >= per_elem / NVLINK_MEASURED:
             roof.update({"bound": "hbm", "achieved": hbm, "frac": hbm_view["frac"],
                          "bytes_per_element": hbm_elem, "nvlink_view": nvl_view})
