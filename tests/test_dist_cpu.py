@@ -72,3 +72,48 @@ def test_dp_groups_from_config4_plan():
     assert [g.index for g in groups] == [0, 1, 2, 3, 0, 1, 2, 3]
     with pytest.raises(hp.InvalidPlanError):
         DPGroup((0, 1), 5)
+
+
+def _scenario_worker(rank, world, port, scen, result_dir):
+    """Config 4 host logic over gloo: every rank places itself in the
+    reference plan, builds its stage's gradient set and joins its DP row's
+    subgroup (collective over the world)."""
+    import json
+
+    from paper_2312_03549_b200.scenario_run import setup_rank
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    sr = setup_rank(hp.load_scenario(scen), rank)
+    # the DP row's subgroup really contains exactly the row's ranks
+    x = torch.tensor([float(rank + 1)])
+    dist.all_reduce(x, group=sr.process_group)
+    # the clip-norm group is the world (one global norm for both stages)
+    y = torch.tensor([1.0])
+    dist.all_reduce(y, group=sr.norm_group)
+    doc = {"stage": sr.placement.stage, "dp_ranks": list(sr.dp_group.ranks), "index": sr.dp_group.index,
+           "params": sr.gradset.total, "row_sum": float(x), "world_sum": float(y),
+           "norm_ranks": list(sr.norm_ranks)}
+    with open(os.path.join(result_dir, f"r{rank}.json"), "w") as f:
+        json.dump(doc, f)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("scen,world", [("gpt13b_pp2_dp2_hybrid.json", 4), ("gpt13b_pp2_dp4_hybrid.json", 8)])
+def test_scenario_ranks_over_gloo(tmp_path, scen, world):
+    import json
+
+    port = free_port()
+    mp.spawn(_scenario_worker, args=(world, port, str(ROOT / "scenarios" / scen), str(tmp_path)),
+             nprocs=world, join=True)
+    docs = [json.loads((tmp_path / f"r{r}.json").read_text()) for r in range(world)]
+    d = world // 2
+    stage_params = {1: 7_497_318_400, 2: 5_609_881_600}      # SURVEY §8a A1 known answers
+    for r, doc in enumerate(docs):
+        row = list(range(0, d)) if r < d else list(range(d, world))
+        assert doc["stage"] == (1 if r < d else 2)            # the IB cluster holds stage 1 ([23, 17])
+        assert doc["dp_ranks"] == row and doc["index"] == row.index(r)
+        assert doc["params"] == stage_params[doc["stage"]]
+        assert doc["row_sum"] == sum(q + 1 for q in row)
+        assert doc["world_sum"] == world and doc["norm_ranks"] == list(range(world))
