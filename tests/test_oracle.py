@@ -168,3 +168,16 @@ def test_layout_json_roundtrip():
     doc = json.loads(L.to_json())
     assert doc["total_numel"] == 1_312_817_152 and len(doc["buckets"]) == 37
     assert doc["buckets"][0]["params"][0] == len(config_gradset("gpt1.3b").numels) - 1
+
+
+def test_sum_slices_equals_reduce_scatter(oracle):
+    """The streaming form the full-size check uses (each rank holds only its
+    own shard of every rank's bucket) is the reduce-scatter, bit for bit."""
+    rng = np.random.default_rng(3)
+    d, n = 4, 4096
+    packs = [oracle.f32_to_bf16(rng.standard_normal(n).astype(np.float32)) for _ in range(d)]
+    sh = n // d
+    for r in range(d):
+        cut = [p[r * sh:(r + 1) * sh] for p in packs]
+        np.testing.assert_array_equal(oracle.sum_slices(cut), oracle.reduce_scatter(packs, r, d))
+        np.testing.assert_array_equal(oracle.sum_slices_f64(cut), oracle.reduce_scatter_f64(packs, r, d))
