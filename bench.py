@@ -384,12 +384,24 @@ def sweep_probe(world: int, rank: int, dev) -> list:
         iters = max(5, min(50, int(2e9 // (numel * 2))))
         doc = measure_bucket(numel, iters, world, rank, dev, comm,
                              cases=("fused_p2p", "fused_nvls", "nccl_rs+ag"))
-        rows.append({"bucket_MB": doc["bucket_MB"],
-                     **{k: {"ms": v["ms"], "busBW_GBps": v["busBW_GBps"]} for k, v in doc["results"].items()
-                        if isinstance(v, dict)}})
+        rows.append(_sweep_row(doc))
     comm.close()
     torch.cuda.empty_cache()
     return rows
+
+
+def _sweep_row(doc: dict) -> dict:
+    """One bucket size of the sweep: time and busBW per case, with busBW as a
+    fraction of the measured (770) and nominal (900 GB/s) NVLink roofline."""
+    row = {"bucket_MB": doc["bucket_MB"]}
+    for k, v in doc["results"].items():
+        if not isinstance(v, dict):
+            continue
+        bus = v.get("busBW_GBps")
+        row[k] = {"ms": v["ms"], "busBW_GBps": bus,
+                  "frac_nvlink": round(bus / NVLINK_MEASURED, 3) if bus else None,
+                  "frac_nvlink_nominal": round(bus / NVLINK_NOMINAL, 3) if bus else None}
+    return row
 
 
 def _guarded(name, fn, world):

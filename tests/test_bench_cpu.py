@@ -36,3 +36,15 @@ def test_reference_arm_non_zero_rank_is_silent():
     r = _run({"WORLD_SIZE": "2", "RANK": "1"})
     assert r.returncode == 0, r.stderr[-2000:]
     assert not [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+
+
+def test_sweep_row_fractions():
+    sys.path.insert(0, str(ROOT))
+    import bench
+
+    row = bench._sweep_row({"bucket_MB": 1024.0, "results": {
+        "fused_p2p": {"ms": 2.5, "busBW_GBps": 616.0}, "adamw_local": {"ms": 0.1, "busBW_GBps": None},
+        "error": 0}})
+    assert row["bucket_MB"] == 1024.0
+    assert row["fused_p2p"] == {"ms": 2.5, "busBW_GBps": 616.0, "frac_nvlink": 0.8, "frac_nvlink_nominal": 0.684}
+    assert row["adamw_local"]["frac_nvlink"] is None and "error" not in row
