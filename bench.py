@@ -677,7 +677,8 @@ def main():
     ap.add_argument("--first-span-numel", type=int, default=None,
                     help="p2p/nvls: threshold of the step's first span (default: min(--span-numel, 32M))")
     ap.add_argument("--param-barriers", type=int, default=1, choices=[0, 1],
-                    help="p2p/nvls: params-ready barrier per span (1) or one end-of-step barrier (0)")
+                    help="p2p/nvls, hook-driven flows (the overlap measurement): params-ready barrier per "
+                         "span (1) or one end-of-step barrier (0); step() always ends with one barrier")
     ap.add_argument("--backend", default="auto")
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")
     ap.add_argument("--no-e2e", action="store_true")
