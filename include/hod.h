@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define HOD_ABI_VERSION 1
+#define HOD_ABI_VERSION 2
 
 /* library-level error codes (outside the cudaError_t / ncclResult_t ranges) */
 #define HOD_OK 0
@@ -42,6 +42,8 @@ extern "C" {
 #define HOD_EALIGN 10002   /* a buffer violates the documented alignment     */
 #define HOD_ETIMEOUT 10003 /* a cross-GPU wait exceeded its spin budget      */
 #define HOD_ENCCL 10004    /* NCCL returned an error (message has details)   */
+#define HOD_ESPAN 10005    /* ranks met at a barrier slot with different tags,
+                              i.e. closed a span over different buckets     */
 
 /* source dtype of a gradient tensor fed to the packer */
 #define HOD_DTYPE_BF16 0
@@ -108,23 +110,11 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
 
 /* Sum of squares of the values the packed bucket would hold (bf16_rne(src*scale),
  * 0 in gaps), read straight from the tensors: HOD_SUMSQ_PARTIALS fixed-grid
- * partials, at most HOD_PACK_MAX_ENTRIES entries.  d == 1 with clipping:
+ * partials (longer tables are split into windows of HOD_PACK_MAX_ENTRIES whose
+ * sums are added per partial slot in window order).  d == 1 with clipping:
  * norm pass (2 B/element) then hod_pack_adamw with the clip coefficient. */
 int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel,
                    float scale, int src_dtype, float* partials, void* stream);
-
-/* ---- K1 + reduce-scatter transfer in one kernel (push) ---------------------
- * The pack of hod_pack_bf16 with each packed element stored straight into its
- * OWNER's buffer over NVLink: element i of the bucket (shard q = i / n, n =
- * bucket_numel / d, a multiple of 8) goes to dst_buckets[q][rank*n + i - q*n],
- * i.e. slot `rank` of rank q's bucket region.  dst_buckets[q] = the peer-mapped
- * address of this bucket's start in rank q's flat grad buffer (dst_buckets[rank]
- * is local).  After every rank's push (and a barrier) each rank reduces its d
- * slots locally (hod_p2p_span.staged = 1): the RS bytes cross NVLink during the
- * pack — during backward — instead of in the update kernel. */
-int hod_pack_push(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel,
-                  float scale, int src_dtype, uint16_t* const* dst_buckets, int d, int rank,
-                  void* stream);
 
 /* ---- K3: deterministic sum of squares of a bf16 shard -----
  * Writes HOD_SUMSQ_PARTIALS fp32 partial sums to partials[0..HOD_SUMSQ_PARTIALS)
@@ -216,7 +206,8 @@ int hod_all_reduce_f32(float* buf, size_t n, void* comm, void* stream);
 typedef struct hod_p2p_span {
   uint16_t* grad[HOD_P2P_MAX_RANKS];  /* rank q's flat grad-bucket buffer; nvls: [0] = multicast base */
   uint16_t* param[HOD_P2P_MAX_RANKS]; /* rank q's flat param buffer; nvls: [0] = multicast base */
-  uint32_t* flags[HOD_P2P_MAX_RANKS]; /* rank q's flag array: [slot][HOD_P2P_MAX_RANKS] u32 */
+  uint64_t* flags[HOD_P2P_MAX_RANKS]; /* rank q's flag array: [slot][HOD_P2P_MAX_RANKS] u64,
+                                         value = epoch << 32 | tag */
   uint16_t* local_grad;   /* this rank's flat grad buffer: the reduced bf16 shard of bucket k is
                              kept in place at bucket_start[k] + rank*shard_numel[k] (RS: out,
                              ADAMW_AG: in, FUSED: only when keep_reduced) */
@@ -235,18 +226,24 @@ typedef struct hod_p2p_span {
   int keep_reduced;
   int slot;               /* barrier slot (index of the span's first bucket) */
   uint32_t epoch;         /* monotonically increasing per step, > 0 */
+  uint32_t tag;           /* span identity checked at the barrier (HOD_SPAN_TAG(first, last)):
+                             a peer arriving at `slot` with the same epoch and another tag
+                             records HOD_ESPAN in *err and the launch skips its work */
   unsigned long long timeout_ns; /* barrier spin budget (0 = 20 s) */
-  int staged;             /* 1: the reduce-scatter was pushed by hod_pack_push — slot q of
-                             bucket k's region in local_grad (bucket_start[k] + q*shard_numel[k])
-                             holds rank q's part of this rank's shard; RS/FUSED read the d slots
-                             locally (same rank-order sum, same bits as the pull); grad[] unused.
-                             p2p all-gather only (nvls must be 0). */
 } hod_p2p_span;
 
+#define HOD_SPAN_TAG(first, last) ((uint32_t)(first) | ((uint32_t)(last) << 16))
+#define HOD_NORM_TAG 0x4e4f524du /* tag of the norm-exchange barrier */
+
+/* Errors inside a launch go to the device word *err (HOD_ETIMEOUT, HOD_ESPAN).
+ * Fail-stop: once *err is nonzero every later barrier, span and update launch
+ * of this rank returns at entry without signalling its peers (which then time
+ * out in turn); the host reads the word and raises. */
 int hod_p2p_step(const hod_p2p_span* span, int mode, const hod_adamw_params* hp, void* stream);
 
-/* stand-alone cross-GPU barrier on `slot` (1 CTA): signal then wait for all d ranks */
-int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+/* stand-alone cross-GPU barrier on `slot` (1 CTA): signal (epoch, tag) then wait
+ * for all d ranks; a different tag at the same epoch records HOD_ESPAN */
+int hod_p2p_barrier(uint64_t* const* flags, int d, int rank, int slot, uint32_t epoch, uint32_t tag,
                     unsigned long long timeout_ns, uint32_t* err, void* stream);
 
 /* One-directional hand-off between two GPUs (pipeline activations, §8f.3):
@@ -261,7 +258,7 @@ int hod_p2p_wait(const uint32_t* flag, uint32_t epoch, unsigned long long timeou
  * partials, publish to xchg[q][rank] (fp64) of every rank, barrier, rank-order
  * sum => identical deterministic coef/norm on all ranks. */
 int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg,
-                 uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+                 uint64_t* const* flags, int d, int rank, int slot, uint32_t epoch,
                  unsigned long long timeout_ns, uint32_t* err, float max_norm, float* coef,
                  float* norm, float* sumsq, void* stream);
 

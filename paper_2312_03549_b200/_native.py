@@ -23,7 +23,7 @@ HOD_DTYPE_F32 = 1
 # every symbol include/hod.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
-    "hod_pack_bf16", "hod_pack_push", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
+    "hod_pack_bf16", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
     "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma", "hod_adamw", "hod_sumsq",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
@@ -38,6 +38,15 @@ class PackEntry(ctypes.Structure):
 HOD_P2P_MAX_RANKS = 8
 HOD_P2P_FUSED, HOD_P2P_RS, HOD_P2P_ADAMW_AG = 0, 1, 2
 HOD_P2P_MAX_SPAN = 32
+HOD_NORM_TAG = 0x4E4F524D
+HOD_ETIMEOUT, HOD_ESPAN = 10003, 10005
+ERROR_NAMES = {HOD_ETIMEOUT: "cross-GPU barrier timeout (a peer never arrived)",
+               HOD_ESPAN: "span mismatch (peers closed a span over different buckets)"}
+
+
+def span_tag(first: int, last: int) -> int:
+    """HOD_SPAN_TAG(first, last) of include/hod.h."""
+    return (first & 0xFFFF) | ((last & 0xFFFF) << 16)
 
 
 class P2PSpan(ctypes.Structure):
@@ -54,8 +63,7 @@ class P2PSpan(ctypes.Structure):
         ("shard_numel", ctypes.c_int64 * HOD_P2P_MAX_SPAN),
         ("n_buckets", ctypes.c_int), ("d", ctypes.c_int), ("rank", ctypes.c_int), ("nvls", ctypes.c_int),
         ("keep_reduced", ctypes.c_int), ("slot", ctypes.c_int),
-        ("epoch", ctypes.c_uint32), ("timeout_ns", ctypes.c_ulonglong),
-        ("staged", ctypes.c_int),
+        ("epoch", ctypes.c_uint32), ("tag", ctypes.c_uint32), ("timeout_ns", ctypes.c_ulonglong),
     ]
 
 
@@ -64,7 +72,10 @@ class AdamWParams(ctypes.Structure):
                 ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("step", ctypes.c_int64)]
 
 
+ABI_VERSION = 2          # HOD_ABI_VERSION of include/hod.h
+
 _lib = None
+_grid_base = 0
 
 
 def load(build_if_missing: bool = True):
@@ -82,6 +93,10 @@ def load(build_if_missing: bool = True):
         raise DeviceError(f"CUDA library {LIB_PATH} is missing; run "
                           "`python -m paper_2312_03549_b200.build_native`")
     L = ctypes.CDLL(str(LIB_PATH))
+    L.hod_abi_version.restype = ctypes.c_int
+    if L.hod_abi_version() != ABI_VERSION:
+        raise DeviceError(f"{LIB_PATH} has ABI {L.hod_abi_version()}, this package needs {ABI_VERSION}: "
+                          "rebuild with `python -m paper_2312_03549_b200.build_native --force`")
     P, I64, I, F = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float
     sig = {
         "hod_abi_version": ([], I),
@@ -94,7 +109,6 @@ def load(build_if_missing: bool = True):
                             ctypes.POINTER(AdamWParams), P, P], I),
         "hod_sum_partials": ([P, I64, P, P], I),
         "hod_pack_sumsq": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, P], I),
-        "hod_pack_push": ([ctypes.POINTER(PackEntry), I, I64, F, I, P, I, I, P], I),
         "hod_clip_coef": ([P, F, P, P, P], I),
         "hod_adamw_bf16": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
         "hod_adamw": ([P, P, P, P, P, I64, F, F, F, F, F, I64, P, P], I),
@@ -108,7 +122,7 @@ def load(build_if_missing: bool = True):
         "hod_all_gather_bf16": ([P, P, ctypes.c_size_t, P, P], I),
         "hod_all_reduce_f32": ([P, ctypes.c_size_t, P, P], I),
         "hod_p2p_step": ([ctypes.POINTER(P2PSpan), I, ctypes.POINTER(AdamWParams), P], I),
-        "hod_p2p_barrier": ([P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, P], I),
+        "hod_p2p_barrier": ([P, I, I, I, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_ulonglong, P, P], I),
         "hod_p2p_norm": ([P, I64, P, P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, F, P, P, P, P], I),
         "hod_ce_copy": ([P, P, ctypes.c_size_t, P], I),
         "hod_p2p_signal": ([P, ctypes.c_uint32, P], I),
@@ -130,6 +144,20 @@ def check(rc: int, what: str) -> None:
 
 def call(name: str, *args) -> None:
     check(getattr(load(), name)(*args), name)
+
+
+def set_grid_base(max_ctas: int) -> None:
+    """Standing CTA cap of every launch of this thread (0 = none).  The
+    optimizer's temporary ``sm_budget`` caps are taken relative to it and
+    restore it afterwards (emulation.EmulatedRow keeps d ranks' kernels
+    co-resident on one GPU with it)."""
+    global _grid_base
+    call("hod_set_grid_limit", int(max_ctas))
+    _grid_base = int(max_ctas)
+
+
+def grid_base() -> int:
+    return _grid_base
 
 
 def launch_count() -> int:

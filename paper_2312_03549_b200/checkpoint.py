@@ -5,9 +5,11 @@ Each rank writes its own shard files — fp32 master, exp_avg, exp_avg_sq (the
 manifest with the ``BucketLayout``, the step count, the hyper-parameters and
 a sha256 per array, in the same determinism conventions as the reference's
 scenario fingerprint (config.py:292: sha256 of raw bytes).  Loading checks
-that the layout and the DP position match and restores the bf16 params from
-the master (an all-gather of the restored shards for d > 1 happens on the
-next step, or via ``load(..., gather=True)``).
+that the layout and the DP position match, restores the local bf16 param
+shards from the master and, with ``gather=True`` (the default), all-gathers
+them so every rank's param buffer holds the restored model before the next
+forward (``DistributedOptimizer.gather_params``; every rank of the row must
+call ``load``).
 """
 
 from __future__ import annotations
@@ -54,7 +56,7 @@ def save(opt, directory) -> Path:
     return out
 
 
-def load(opt, directory) -> dict:
+def load(opt, directory, gather: bool = True) -> dict:
     d = Path(directory)
     r = opt.group.global_rank
     man = json.loads((d / f"rank{r:05d}.manifest.json").read_text())
@@ -69,10 +71,12 @@ def load(opt, directory) -> dict:
             raise ConfigError(f"checkpoint array {name} is corrupt (sha256 mismatch)")
         getattr(opt, name).copy_(torch.from_numpy(arr).to(opt.device))
     opt.step_count = int(man["step"])
-    # the local param shard follows from the master; peers' shards arrive with
-    # the next all-gather (d > 1)
+    # the local param shard follows from the master (RNE, as the update
+    # kernels round it); the peers' shards come from their owners
     for b, off in zip(opt.layout.buckets, opt.layout.shard_offsets()):
         lo, hi = b.shard_range(opt.shard_index, opt.dp)
         opt.param_buffer[lo:hi].copy_(opt.master[off:off + (hi - lo)].to(torch.bfloat16))
     torch.cuda.synchronize(opt.device)
+    if gather and opt.dp > 1:
+        opt.gather_params()
     return man

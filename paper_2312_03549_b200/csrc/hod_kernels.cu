@@ -148,66 +148,6 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------------------
-// K1 + RS transfer (push): the pack above, each 8-element vector stored into
-// its owner's slot over NVLink.  Window-relative element i is bucket element
-// lo + i; owner q = (lo + i) / n; destination = dst[q] + rank*n + (lo+i - q*n).
-// Shards are multiples of 8 elements, so a vector never straddles owners.
-// ---------------------------------------------------------------------------
-struct PushArgs {
-  uint16_t* dst[HOD_P2P_MAX_RANKS];  // bucket start on rank q (peer-mapped)
-  int64_t n;                         // shard numel
-  int64_t lo;                        // window start within the bucket
-  int d;
-  int rank;
-};
-
-__device__ __forceinline__ uint16_t* push_addr(const PushArgs& pa, int64_t i) {
-  const int64_t I = pa.lo + i;
-  int q = 0;
-#pragma unroll
-  for (int k = 1; k < HOD_P2P_MAX_RANKS; ++k) q += (k < pa.d && I >= k * pa.n) ? 1 : 0;
-  return pa.dst[q] + (static_cast<int64_t>(pa.rank) - q) * pa.n + I;
-}
-
-template <typename SrcT>
-__global__ void __launch_bounds__(kThreads) pack_push_kernel(const __grid_constant__ PackTable t,
-                                                              const __grid_constant__ PushArgs pa,
-                                                              int64_t span, float scale) {
-  pdl_trigger();
-  const int64_t n_tiles = (span + kPackTile - 1) / kPackTile;
-  int e = 0;
-  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const int64_t a = tile * kPackTile;
-    const int64_t b = min(a + kPackTile, span);
-    while (e < t.n && t.off[e] + t.numel[e] <= a) ++e;
-    const bool inside = e < t.n && t.off[e] <= a && b <= t.off[e] + t.numel[e];
-    if (inside && ((t.vec_ok >> e) & 1ull) && (b - a) == kPackTile) {
-      const int64_t s0 = a - t.off[e];
-      float f[kPackUnroll][8];
-#pragma unroll
-      for (int u = 0; u < kPackUnroll; ++u)
-        load8<SrcT>(t.src[e], s0 + (static_cast<int64_t>(u) * kThreads + threadIdx.x) * kPackVec, f[u]);
-#pragma unroll
-      for (int u = 0; u < kPackUnroll; ++u) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) f[u][k] = __fmul_rn(f[u][k], scale);
-        const int64_t i = a + (static_cast<int64_t>(u) * kThreads + threadIdx.x) * kPackVec;
-        *reinterpret_cast<uint4*>(push_addr(pa, i)) = pack8(f[u]);
-      }
-    } else {
-      int ei = e;
-      for (int64_t i = a + threadIdx.x; i < b; i += kThreads) {
-        while (ei < t.n && t.off[ei] + t.numel[ei] <= i) ++ei;
-        float x = 0.0f;
-        if (ei < t.n && t.off[ei] <= i) x = __fmul_rn(load_src<SrcT>(t.src[ei], i - t.off[ei]), scale);
-        *push_addr(pa, i) = (ei < t.n && t.off[ei] <= i) ? f32_to_bf16(x) : static_cast<uint16_t>(0);
-      }
-    }
-  }
-  __threadfence_system();  // pushed bytes performed before any later signal
-}
-
-// ---------------------------------------------------------------------------
 // K1+K2 fused (d == 1, no collective between them): the update reads the
 // gradient straight from the per-parameter tensors through the pack table,
 // with the same scale-then-RNE-to-bf16 the bucket would have held, so the
@@ -413,7 +353,8 @@ __global__ void __launch_bounds__(kSumsqThreads) sumsq_kernel(const uint16_t* __
 template <typename SrcT>
 __global__ void __launch_bounds__(kSumsqThreads) pack_sumsq_kernel(const __grid_constant__ PackTable t,
                                                                     int64_t numel, float scale,
-                                                                    float* __restrict__ partials) {
+                                                                    float* __restrict__ partials,
+                                                                    int accumulate) {
   constexpr int kThreads = kSumsqThreads;
   constexpr int kPackTile = kSumsqTile;
   pdl_trigger();  // the next bucket's norm pass writes other partial slots
@@ -462,8 +403,10 @@ __global__ void __launch_bounds__(kSumsqThreads) pack_sumsq_kernel(const __grid_
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc = __fadd_rn(acc, acc8[k]);
   const float sblk = block_sum<kSumsqThreads>(acc);
-  if (threadIdx.x == 0) partials[blockIdx.x] = sblk;
-  if (blockIdx.x == 0)
+  // windows after the first of a > HOD_PACK_MAX_ENTRIES table add onto the
+  // partials of the windows before them (fixed window order: reproducible)
+  if (threadIdx.x == 0) partials[blockIdx.x] = accumulate ? __fadd_rn(partials[blockIdx.x], sblk) : sblk;
+  if (blockIdx.x == 0 && !accumulate)
     for (int i = gridDim.x + threadIdx.x; i < HOD_SUMSQ_PARTIALS; i += blockDim.x) partials[i] = 0.0f;
 }
 
@@ -591,41 +534,6 @@ int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket
   });
 }
 
-int hod_pack_push(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel, float scale,
-                  int src_dtype, uint16_t* const* dst_buckets, int d, int rank, void* stream) {
-  if (!dst_buckets || d < 1 || d > HOD_P2P_MAX_RANKS || rank < 0 || rank >= d) {
-    set_error("hod_pack_push: bad group (d=%d rank=%d)", d, rank); return HOD_EINVAL;
-  }
-  if (bucket_numel % (8LL * d)) {
-    set_error("hod_pack_push: bucket_numel %lld not a multiple of 8*d", (long long)bucket_numel);
-    return HOD_EALIGN;
-  }
-  PushArgs pa;
-  memset(&pa, 0, sizeof(pa));
-  for (int q = 0; q < d; ++q) {
-    pa.dst[q] = dst_buckets[q];
-    if (!pa.dst[q] || !aligned16(pa.dst[q])) {
-      set_error("hod_pack_push: destination %d null or not 16-byte aligned", q); return HOD_EALIGN;
-    }
-  }
-  pa.n = bucket_numel / d;
-  pa.d = d;
-  pa.rank = rank;
-  if ((pa.n * 2) % 16) { set_error("hod_pack_push: shard not a multiple of 8 elements"); return HOD_EALIGN; }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  return for_each_window("hod_pack_push", entries, n_entries, bucket_numel, src_dtype,
-                         [&](const PackTable& t, int64_t lo, int64_t span) {
-    pa.lo = lo;
-    const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, src_dtype == HOD_DTYPE_BF16 ? 16 : 3);
-    count_launch(1);
-    if (src_dtype == HOD_DTYPE_BF16)
-      launch_pdl(pack_push_kernel<uint16_t>, grid, kThreads, s, t, pa, span, scale);
-    else
-      launch_pdl(pack_push_kernel<float>, grid, kThreads, s, t, pa, span, scale);
-    return cuda_status(cudaGetLastError(), "hod_pack_push launch");
-  });
-}
-
 int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel, float scale,
                    int src_dtype, float* master, float* exp_avg, float* exp_avg_sq, uint16_t* param,
                    const hod_adamw_params* hp, const float* clip_coef, void* stream) {
@@ -666,18 +574,28 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
 int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_numel, float scale,
                    int src_dtype, float* partials, void* stream) {
   if (!partials) { set_error("hod_pack_sumsq: null partials"); return HOD_EINVAL; }
-  if (n_entries > HOD_PACK_MAX_ENTRIES) {
-    set_error("hod_pack_sumsq: at most %d entries per call", HOD_PACK_MAX_ENTRIES); return HOD_EINVAL;
-  }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (bucket_numel == 0) return hod_sumsq_bf16(nullptr, 0, partials, stream);
+  int window = 0;
   return for_each_window("hod_pack_sumsq", entries, n_entries, bucket_numel, src_dtype,
                          [&](const PackTable& t, int64_t lo, int64_t span) {
     count_launch(1);
-    if (src_dtype == HOD_DTYPE_BF16)
-      launch_pdl(pack_sumsq_kernel<uint16_t>, partials_grid(), kSumsqThreads, s, t, span, scale, partials);
-    else
-      launch_pdl(pack_sumsq_kernel<float>, partials_grid(), kSumsqThreads, s, t, span, scale, partials);
+    // window 0 writes the fixed-grid partials; later windows of a long table
+    // accumulate onto them, so they must see window 0's result: full stream
+    // dependency (no PDL) for them.  Every window triggers its own dependents
+    // at entry: the next bucket's norm pass writes other partial slots.
+    const int acc = window++ > 0;
+    const int grid = partials_grid();
+    if (!acc) {
+      if (src_dtype == HOD_DTYPE_BF16)
+        launch_pdl(pack_sumsq_kernel<uint16_t>, grid, kSumsqThreads, s, t, span, scale, partials, 0);
+      else
+        launch_pdl(pack_sumsq_kernel<float>, grid, kSumsqThreads, s, t, span, scale, partials, 0);
+    } else if (src_dtype == HOD_DTYPE_BF16) {
+      pack_sumsq_kernel<uint16_t><<<grid, kSumsqThreads, 0, s>>>(t, span, scale, partials, 1);
+    } else {
+      pack_sumsq_kernel<float><<<grid, kSumsqThreads, 0, s>>>(t, span, scale, partials, 1);
+    }
     (void)lo;
     return cuda_status(cudaGetLastError(), "hod_pack_sumsq launch");
   });

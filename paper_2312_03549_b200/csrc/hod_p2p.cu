@@ -24,12 +24,19 @@
 //       the reduced bf16 shard lives in place in the own-shard region of the
 //       local grad buffer (only this rank ever reads that region).
 //
-// Barriers are monotonic epoch flags: rank r writes `epoch` into slot
-// [slot][r] of every peer's flag array (st.release.sys) and waits until its own
-// [slot][q] >= epoch for all q (ld.acquire.sys).  Every CTA signals (idempotent
-// store), so progress never depends on which CTAs are resident.  Spins are
-// bounded by a %globaltimer budget; on timeout the kernel records HOD_ETIMEOUT
-// in the caller's device error word and skips its work instead of hanging.
+// Barriers are monotonic epoch flags: rank r writes (epoch << 32 | tag) into
+// slot [slot][r] of every peer's 64-bit flag array (st.release.sys) and waits
+// until its own [slot][q] carries an epoch >= `epoch` for all q
+// (ld.acquire.sys).  The tag names what the slot synchronises (a span's first
+// and last bucket): a peer that arrives with the same epoch but another tag
+// closed its span differently, which records HOD_ESPAN instead of reading a
+// bucket the peer has not packed.  Every CTA signals (idempotent store), so
+// progress never depends on which CTAs are resident.  Spins are bounded by a
+// %globaltimer budget; on timeout the kernel records HOD_ETIMEOUT in the
+// caller's device error word and skips its work instead of hanging.  Once the
+// error word is set, every later barrier / update of the rank skips at entry
+// without signalling (fail-stop: peers time out in turn, no rank proceeds on
+// a half-finished step; the host surfaces the word as DeviceError).
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -52,16 +59,15 @@ struct PeerTable {
 enum : int {
   kSrcPeer = 0,    // pull from the d peers' packed buckets (p2p)
   kSrcNvls = 1,    // one multimem.ld_reduce through the switch (nvls; AG via multimem.st)
-  kSrcStaged = 2,  // pushed into the local buffer by hod_pack_push (slot q of the
-                   // bucket region holds rank q's part of this rank's shard)
 };
 
 struct BarrierArgs {
-  PeerTable flags;          // flags[q] = base of rank q's flag array (device ptrs)
-  uint32_t* local_flags;    // this rank's flag array
+  PeerTable flags;          // flags[q] = base of rank q's 64-bit flag array (device ptrs)
+  uint64_t* local_flags;    // this rank's flag array
   uint32_t* err;            // device error word (nullable)
   int slot;
   uint32_t epoch;
+  uint32_t tag;             // what the slot synchronises (must agree across ranks)
   unsigned long long timeout_ns;
 };
 
@@ -76,7 +82,6 @@ struct SpanArgs {
   const float* coef;        // optional clip coefficient (device)
   int64_t own_off[kMaxSpan];     // element offset of this rank's shard of bucket k
   int64_t elem_end[kMaxSpan];    // prefix (inclusive) of shard elements over the span
-  int64_t shard_n[kMaxSpan];     // shard numel of bucket k (staged slot stride)
   int64_t chunk_end[kMaxSpan];   // prefix (inclusive) of 256-element chunks per bucket shard
   int n_buckets;
   int d;
@@ -99,29 +104,52 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   return v;
 }
 
+__device__ __forceinline__ void st_release_sys64(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_acquire_sys64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Nonzero once any kernel of this rank recorded an error (fail-stop check at
+// kernel entry; one load per CTA).
+__device__ __forceinline__ bool rank_failed(const uint32_t* err) {
+  return err && *reinterpret_cast<const volatile uint32_t*>(err) != 0u;
+}
+
 // Signal arrival at `slot` to every rank and wait for all of them.  Returns
-// false (and records the error) on timeout.  Must be called by all threads.
+// false (and records the error) on timeout or tag mismatch, and at once —
+// without signalling — if the rank already failed.  Called by all threads.
 __device__ bool cross_gpu_barrier(const BarrierArgs& b, int d, int rank) {
-  __shared__ int timed_out;
-  if (threadIdx.x == 0) timed_out = 0;
+  __shared__ int failed;
+  if (threadIdx.x == 0) failed = rank_failed(b.err) ? 1 : 0;
   __syncthreads();
+  if (failed) return false;
   if (threadIdx.x < d) {
     const int q = threadIdx.x;
-    uint32_t* peer = reinterpret_cast<uint32_t*>(b.flags.p[q]) + b.slot * kMaxRanks + rank;
-    st_release_sys(peer, b.epoch);
-    const uint32_t* mine = b.local_flags + b.slot * kMaxRanks + q;
+    uint64_t* peer = reinterpret_cast<uint64_t*>(b.flags.p[q]) + b.slot * kMaxRanks + rank;
+    st_release_sys64(peer, (static_cast<uint64_t>(b.epoch) << 32) | b.tag);
+    const uint64_t* mine = b.local_flags + b.slot * kMaxRanks + q;
     const unsigned long long t0 = globaltimer();
-    while (static_cast<int32_t>(ld_acquire_sys(mine) - b.epoch) < 0) {
+    uint64_t v;
+    while (static_cast<int32_t>(static_cast<uint32_t>((v = ld_acquire_sys64(mine)) >> 32) - b.epoch) < 0) {
       if (globaltimer() - t0 > b.timeout_ns) {
-        atomicExch(&timed_out, 1);
+        atomicExch(&failed, 1);
         if (b.err) atomicExch(b.err, static_cast<uint32_t>(HOD_ETIMEOUT));
         break;
       }
       __nanosleep(100);
     }
+    if (!failed && static_cast<uint32_t>(v >> 32) == b.epoch && static_cast<uint32_t>(v) != b.tag) {
+      atomicExch(&failed, 1);
+      if (b.err) atomicExch(b.err, static_cast<uint32_t>(HOD_ESPAN));
+    }
   }
   __syncthreads();
-  return timed_out == 0;
+  return failed == 0;
 }
 
 __device__ __forceinline__ float block_sum_f(float x) {
@@ -173,7 +201,6 @@ struct Item {
   float4 st[2][3];     // per quad: master, m, v
   int64_t e[2];        // element offset in the flat buffers
   int64_t s[2];        // element offset in the span's state
-  int64_t sn[2];       // shard numel of the quad's bucket (staged slot stride)
   bool ok[2];
 };
 
@@ -192,7 +219,7 @@ __device__ __forceinline__ void locate_chunk(const SpanArgs& a, int64_t ch, int 
   while (k < a.n_buckets - 1 && ch >= a.chunk_end[k]) ++k;
   const int64_t first_chunk = k ? a.chunk_end[k - 1] : 0;
   const int64_t first_elem = k ? a.elem_end[k - 1] : 0;
-  const int64_t n = a.shard_n[k];
+  const int64_t n = a.elem_end[k] - first_elem;
   const int64_t own = a.own_off[k];
   const int64_t base = (ch - first_chunk) * kChunk + lane * 4;
   it.e8 = own + (ch - first_chunk) * kChunk + lane * 8;
@@ -203,7 +230,6 @@ __device__ __forceinline__ void locate_chunk(const SpanArgs& a, int64_t ch, int 
     it.ok[h] = off < n;
     it.e[h] = own + off;
     it.s[h] = first_elem + off;
-    it.sn[h] = n;
   }
 }
 
@@ -226,13 +252,6 @@ __device__ __forceinline__ void load_item(const SpanArgs& a, Item<D, kSrc, W>& i
       it.raw[h][0] = *reinterpret_cast<const uint2*>(a.local_grad + e);
     } else if constexpr (kSrc == kSrcNvls) {
       it.raw[h][0] = ld_reduce_bf16x4(reinterpret_cast<const uint16_t*>(a.grad.p[0]) + e);
-    } else if constexpr (kSrc == kSrcStaged) {
-      // slot q of the bucket region = e + (q - rank) * shard numel, all local
-      const int dd = D > 0 ? D : a.d;
-      const uint16_t* base = a.local_grad + e - static_cast<int64_t>(rank) * it.sn[h];
-#pragma unroll
-      for (int q = 0; q < ItemT::kRaw; ++q)
-        if (q < dd) it.raw[h][q] = *reinterpret_cast<const uint2*>(base + q * it.sn[h]);
     } else if constexpr (!ItemT::kWide) {
       const int dd = D > 0 ? D : a.d;
 #pragma unroll
@@ -350,6 +369,13 @@ __global__ void __launch_bounds__(kThreads, HOD_P2P_MINB) p2p_step_kernel(const 
                                                              int rank) {
   if (kMode != 2) {
     if (!cross_gpu_barrier(b, a.d, rank)) return;
+  } else {
+    // the update half has no barrier of its own: it must not apply a clip
+    // coefficient left over from a norm exchange that failed
+    __shared__ int failed;
+    if (threadIdx.x == 0) failed = rank_failed(b.err);
+    __syncthreads();
+    if (failed) return;
   }
   const float coef = (kMode == 2 && a.coef) ? __ldg(a.coef) : 1.0f;
   const int64_t n_chunks = a.chunk_end[a.n_buckets - 1];
@@ -483,7 +509,7 @@ static void dispatch_d(const SpanArgs& a, const BarrierArgs& b, const AdamWConst
   }
 }
 
-static int fill_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+static int fill_barrier(uint64_t* const* flags, int d, int rank, int slot, uint32_t epoch, uint32_t tag,
                         unsigned long long timeout_ns, uint32_t* err, BarrierArgs* b) {
   memset(b, 0, sizeof(*b));
   for (int q = 0; q < d; ++q) {
@@ -494,6 +520,7 @@ static int fill_barrier(uint32_t* const* flags, int d, int rank, int slot, uint3
   b->err = err;
   b->slot = slot;
   b->epoch = epoch;
+  b->tag = tag;
   b->timeout_ns = timeout_ns ? timeout_ns : 20000000000ull;
   return HOD_OK;
 }
@@ -508,15 +535,11 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
     return HOD_EINVAL;
   }
   memset(a, 0, sizeof(*a));
-  if (sp->staged && sp->nvls) {
-    set_error("hod_p2p: staged (pushed) reduce-scatter pairs with the p2p all-gather only");
-    return HOD_EINVAL;
-  }
   const int nptr = sp->nvls ? 1 : sp->d;
   for (int q = 0; q < nptr; ++q) {
     a->grad.p[q] = reinterpret_cast<uintptr_t>(sp->grad[q]);
     a->param.p[q] = reinterpret_cast<uintptr_t>(sp->param[q]);
-    if ((!sp->staged && !a->grad.p[q]) || !a->param.p[q] || (a->grad.p[q] & 15) || (a->param.p[q] & 15)) {
+    if (!a->grad.p[q] || !a->param.p[q] || (a->grad.p[q] & 15) || (a->param.p[q] & 15)) {
       set_error("hod_p2p: peer buffer %d null or not 16-byte aligned", q);
       return HOD_EALIGN;
     }
@@ -533,7 +556,6 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
       return HOD_EALIGN;
     }
     a->own_off[k] = sp->bucket_start[k] + static_cast<int64_t>(sp->rank) * n;
-    a->shard_n[k] = n;
     a->chunk_end[k] = (k ? a->chunk_end[k - 1] : 0) + (n + kChunk - 1) / kChunk;
     elems += n;
     a->elem_end[k] = elems;
@@ -546,7 +568,7 @@ static int fill_span(const hod_p2p_span* sp, SpanArgs* a, BarrierArgs* b) {
   a->n_buckets = sp->n_buckets;
   a->d = sp->d;
   a->keep_reduced = sp->keep_reduced;
-  return fill_barrier(sp->flags, sp->d, sp->rank, sp->slot, sp->epoch, sp->timeout_ns, sp->err, b);
+  return fill_barrier(sp->flags, sp->d, sp->rank, sp->slot, sp->epoch, sp->tag, sp->timeout_ns, sp->err, b);
 }
 
 }  // namespace hod
@@ -573,15 +595,12 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
   }();
   const int grid = (mode == HOD_P2P_RS) ? partials_grid() : grid_for(chunks * 32, kThreads, p2p_cps);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  // staged RS reads locally; its AG goes peer to peer (p2p stores)
-  const int src = sp->staged ? kSrcStaged : (sp->nvls ? kSrcNvls : kSrcPeer);
+  const int src = sp->nvls ? kSrcNvls : kSrcPeer;
   if (mode == HOD_P2P_FUSED) {
     if (src == kSrcNvls) dispatch_d<kSrcNvls, 0>(a, b, c, sp->rank, grid, s);
-    else if (src == kSrcStaged) dispatch_d<kSrcStaged, 0>(a, b, c, sp->rank, grid, s);
     else dispatch_d<kSrcPeer, 0>(a, b, c, sp->rank, grid, s);
   } else if (mode == HOD_P2P_RS) {
     if (src == kSrcNvls) dispatch_d<kSrcNvls, 1>(a, b, c, sp->rank, grid, s);
-    else if (src == kSrcStaged) dispatch_d<kSrcStaged, 1>(a, b, c, sp->rank, grid, s);
     else dispatch_d<kSrcPeer, 1>(a, b, c, sp->rank, grid, s);
   } else {
     // the update half never reads the grad side: only the AG flavour matters
@@ -607,20 +626,20 @@ int hod_p2p_wait(const uint32_t* flag, uint32_t epoch, unsigned long long timeou
   return cuda_status(cudaGetLastError(), "hod_p2p_wait launch");
 }
 
-int hod_p2p_barrier(uint32_t* const* flags, int d, int rank, int slot, uint32_t epoch,
+int hod_p2p_barrier(uint64_t* const* flags, int d, int rank, int slot, uint32_t epoch, uint32_t tag,
                     unsigned long long timeout_ns, uint32_t* err, void* stream) {
   if (!flags || d < 1 || d > kMaxRanks || rank < 0 || rank >= d || slot < 0) {
     set_error("hod_p2p_barrier: bad arguments"); return HOD_EINVAL;
   }
   BarrierArgs b;
-  int rc = fill_barrier(flags, d, rank, slot, epoch, timeout_ns, err, &b);
+  int rc = fill_barrier(flags, d, rank, slot, epoch, tag, timeout_ns, err, &b);
   if (rc) return rc;
   count_launch(1);
   barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(b, d, rank);
   return cuda_status(cudaGetLastError(), "hod_p2p_barrier launch");
 }
 
-int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg, uint32_t* const* flags,
+int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg, uint64_t* const* flags,
                  int d, int rank, int slot, uint32_t epoch, unsigned long long timeout_ns, uint32_t* err,
                  float max_norm, float* coef, float* norm, float* sumsq, void* stream) {
   if (!partials || !xchg || !flags || !coef || d < 1 || d > kMaxRanks || rank < 0 || rank >= d ||
@@ -631,7 +650,7 @@ int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg,
   memset(&x, 0, sizeof(x));
   for (int q = 0; q < d; ++q) x.p[q] = reinterpret_cast<uintptr_t>(xchg[q]);
   BarrierArgs b;
-  int rc = fill_barrier(flags, d, rank, slot, epoch, timeout_ns, err, &b);
+  int rc = fill_barrier(flags, d, rank, slot, epoch, HOD_NORM_TAG, timeout_ns, err, &b);
   if (rc) return rc;
   count_launch(1);
   norm_exchange_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(

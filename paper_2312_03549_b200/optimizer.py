@@ -43,7 +43,7 @@ import torch
 from . import _native as nat
 from .buckets import BucketLayout, build_bucket_layout
 from .comm import DPGroup, NcclComm
-from .errors import InfeasibleConfigError
+from .errors import DeviceError, InfeasibleConfigError
 
 # fused pack+AdamW launches are chained with programmatic dependent launch
 # unless HOD_PDL=0 (read by the library too, csrc/hod_kernels.cu)
@@ -51,6 +51,7 @@ _PDL = os.environ.get("HOD_PDL", "1") != "0"
 
 _BF16 = torch.bfloat16
 BACKENDS = ("none", "nccl", "p2p", "nvls")
+_SPAN_MAX_BUCKETS = 0xFFFF   # bucket indices fit the 16-bit halves of a span tag
 
 
 @dataclass
@@ -65,9 +66,16 @@ class StepReport:
     clip_coef: torch.Tensor | None = None
     start: torch.cuda.Event | None = None
     end: torch.cuda.Event | None = None
+    err: torch.Tensor | None = None   # device error word of the fused collectives
     resolved: dict = field(default_factory=dict)
 
     def resolve(self) -> dict:
+        """Wait for the step and return its figures; raises DeviceError if a
+        cross-GPU barrier of the step timed out or met a mismatched span."""
+        if self.end is not None:
+            self.end.synchronize()
+        if self.err is not None:
+            raise_device_error(int(self.err.item()))
         if not self.resolved:
             doc = {"step": self.step, "buckets": self.buckets,
                    "params_updated": self.params_updated}
@@ -78,6 +86,13 @@ class StepReport:
                 doc["clip_coef"] = float(self.clip_coef.item())
             self.resolved = doc
         return self.resolved
+
+
+def raise_device_error(code: int) -> None:
+    """DeviceError for a nonzero device error word (include/hod.h HOD_E*)."""
+    if code:
+        raise DeviceError(f"fused collective failed on the device: code {code} "
+                          f"({nat.ERROR_NAMES.get(code, 'unknown')}); the step's update was skipped")
 
 
 def _ptr(t: torch.Tensor) -> int:
@@ -121,6 +136,12 @@ class DistributedOptimizer:
     norm_ranks : ranks over which the clip norm is summed (default: the DP
         row; the whole world for PP x DP so every stage sees one norm).
     grad_scale : multiplier fused into the pack (default 1/d: gradient mean).
+    symmetric, norm_symmetric : factories ``(numel, dtype, device, zero) ->``
+        symmetric buffer (``.tensor``, ``.peer(q)``, ``.multicast()``, ``.mc``,
+        ``.rank``, ``.world``) for the DP row / the clip-norm ranks; default:
+        torch symmetric memory over the process group (symm.SymmetricTensor).
+        ``emulation.EmulatedRow`` supplies one-GPU stand-ins that run the same
+        protocol with d ranks on one device.
     """
 
     def __init__(self, init_params, *, lr: float = 1e-4, betas=(0.9, 0.95), eps: float = 1e-8,
@@ -131,7 +152,7 @@ class DistributedOptimizer:
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
                  sm_budget: int | None = None, span_numel: int = 256 * 2**20,
                  param_barriers: bool = True, pre_barrier: bool | None = None,
-                 rs_push: bool | None = None, first_span_numel: int | None = None):
+                 first_span_numel: int | None = None, symmetric=None, norm_symmetric=None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         init_params = list(init_params)
@@ -198,13 +219,6 @@ class DistributedOptimizer:
             pre_barrier = env == "1"
         self._pre_barrier_auto = pre_barrier is None
         self.pre_barrier = bool(pre_barrier)
-        # p2p reduce-scatter by PUSH (hod_pack_push: the pack stores each
-        # element into its owner's slot over NVLink, the span kernel reduces
-        # locally) instead of PULL (pack locally, span kernel loads from peers)
-        env = os.environ.get("HOD_RS_PUSH")
-        if env is not None:
-            rs_push = env == "1"
-        self.rs_push = bool(rs_push) if rs_push is not None else False
         self._pending_span: list[int] = []
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
@@ -217,17 +231,24 @@ class DistributedOptimizer:
         dev = self.device
         nb = len(L.buckets)
         self._sym = None
+        if nb > _SPAN_MAX_BUCKETS:
+            raise InfeasibleConfigError(f"{nb} buckets: at most {_SPAN_MAX_BUCKETS} (raise bucket_size)")
+        self._emulated = symmetric is not None
         if backend in ("p2p", "nvls"):
-            from .symm import SymmetricTensor, group_for
+            if symmetric is None:
+                from .symm import SymmetricTensor, group_for
 
-            pg = process_group if process_group is not None else group_for(self.group.ranks)
-            self._pg = pg
-            self._sym_grad = SymmetricTensor(total, _BF16, dev, pg)
-            self._sym_param = SymmetricTensor(total, _BF16, dev, pg, zero=True)
-            # barrier flags: slots 0..nb-1 per bucket, nb = end-of-step
-            # barrier slots: [0, nb) span arrival, nb end of step, nb+1+b span done
-            self._sym_flags = SymmetricTensor((2 * nb + 1) * nat.HOD_P2P_MAX_RANKS, torch.int32, dev, pg,
-                                              zero=True)
+                pg = process_group if process_group is not None else group_for(self.group.ranks)
+                self._pg = pg
+
+                def symmetric(numel, dtype, device, zero=False, _pg=pg):
+                    return SymmetricTensor(numel, dtype, device, _pg, zero=zero)
+            self._symmetric = symmetric
+            self._sym_grad = symmetric(total, _BF16, dev, False)
+            self._sym_param = symmetric(total, _BF16, dev, True)
+            # 64-bit barrier flags (epoch << 32 | tag), slots: [0, nb) span
+            # arrival, nb end of step, nb+1+b span b's params ready
+            self._sym_flags = symmetric((2 * nb + 1) * nat.HOD_P2P_MAX_RANKS, torch.int64, dev, True)
             if self._sym_grad.rank != self.shard_index:
                 raise InfeasibleConfigError("process group order differs from the DP row order")
             if backend == "nvls" and not (self._sym_grad.mc and self._sym_param.mc):
@@ -236,11 +257,17 @@ class DistributedOptimizer:
                 self.backend = backend = "p2p"
             self.param_buffer = self._sym_param.tensor
             self.grad_buffer = self._sym_grad.tensor
-            self._err = torch.zeros(1, dtype=torch.int32, device=dev)
             self._norm_group = norm_group
         else:
             self.param_buffer = torch.zeros(total, dtype=_BF16, device=dev)
             self.grad_buffer = torch.empty(total, dtype=_BF16, device=dev)
+        # device error word of the fused collectives (HOD_ETIMEOUT / HOD_ESPAN),
+        # read back asynchronously after every step into pinned memory and
+        # checked at the next begin_step without a host synchronisation
+        self._err = torch.zeros(1, dtype=torch.int32, device=dev)
+        self._err_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self._ev_err = torch.cuda.Event()
+        self._err_pending = False
         shard_total = total // self.dp
         self.master = torch.empty(shard_total, dtype=torch.float32, device=dev)
         self.exp_avg = torch.zeros(shard_total, dtype=torch.float32, device=dev)
@@ -291,12 +318,19 @@ class DistributedOptimizer:
         self.norm_ranks = norm_ranks
         if self.clip is not None and len(norm_ranks) > 1:
             if self.backend in ("p2p", "nvls"):
-                from .symm import SymmetricTensor, group_for
+                if norm_ranks == self.group.ranks:
+                    nsym = self._symmetric
+                elif norm_symmetric is not None:
+                    nsym = norm_symmetric
+                else:
+                    from .symm import SymmetricTensor, group_for
 
-                ng = (self._pg if norm_ranks == self.group.ranks
-                      else (self._norm_group if self._norm_group is not None else group_for(norm_ranks)))
-                self._norm_xchg = SymmetricTensor(nat.HOD_P2P_MAX_RANKS, torch.float64, dev, ng, zero=True)
-                self._norm_flags = SymmetricTensor(nat.HOD_P2P_MAX_RANKS, torch.int32, dev, ng, zero=True)
+                    ng = self._norm_group if self._norm_group is not None else group_for(norm_ranks)
+
+                    def nsym(numel, dtype, device, zero=False, _ng=ng):
+                        return SymmetricTensor(numel, dtype, device, _ng, zero=zero)
+                self._norm_xchg = nsym(nat.HOD_P2P_MAX_RANKS, torch.float64, dev, True)
+                self._norm_flags = nsym(nat.HOD_P2P_MAX_RANKS, torch.int64, dev, True)
                 self._norm_rank = self._norm_xchg.rank
                 self._norm_d = self._norm_xchg.world
             else:
@@ -304,20 +338,23 @@ class DistributedOptimizer:
                                   else NcclComm(norm_ranks, self.group.global_rank, "norm"))
         if self.backend in ("p2p", "nvls"):
             torch.cuda.synchronize(dev)
-            import torch.distributed as dist
+            if not self._emulated:
+                import torch.distributed as dist
 
-            dist.barrier()  # every rank's zeroed flags exist before anyone signals
+                dist.barrier()  # every rank's zeroed flags exist before anyone signals
 
         self._ktiming = None
         self._krun = None                # open run of PDL-chained launches (timing)
         self._grads_resident = False
         self._staging = None
         self._ev_staging_free = None
-        self.step_count = 0
+        self.step_count = 0              # AdamW bias-correction step (restored by checkpoint.load)
+        self._epoch = 0                  # barrier epoch: monotonic, never restored
         self._pending_grads: list[dict[int, torch.Tensor]] = []
         self._launched: list[bool] = []
         self._deferred_ag: list[int] = []
         self._in_step = False
+        self._sync_enabled = True
 
     # ------------------------------------------------------------------ API
     def bucket_layout(self) -> BucketLayout:
@@ -326,8 +363,10 @@ class DistributedOptimizer:
     def begin_step(self) -> None:
         if self._in_step:
             raise InfeasibleConfigError("begin_step called twice without finish_step")
+        self.poll_error()
         self._in_step = True
         self.step_count += 1
+        self._epoch += 1
         nb = len(self.layout.buckets)
         self._pending_grads = [dict() for _ in range(nb)]
         self._launched = [False] * nb
@@ -336,7 +375,7 @@ class DistributedOptimizer:
         self._spans_launched = 0
         self._deferred_pa = []
         self._ev_start.record(torch.cuda.current_stream(self.device))
-        if self.dp > 1 and self.step_count > 1:
+        if self.dp > 1 and self._epoch > 1:
             # this step's packs overwrite the grad buckets the previous step's
             # reduce-scatter read (peers included): order them after its
             # params-ready points even if the caller skipped wait_params
@@ -349,9 +388,23 @@ class DistributedOptimizer:
 
     def grad_ready(self, param_index: int, grad: torch.Tensor) -> None:
         """Backward produced ``grad`` for parameter ``param_index`` (call from a
-        post-accumulate-grad hook).  Launches the bucket once it is complete."""
+        post-accumulate-grad hook).  Launches the bucket once it is complete.
+
+        Each parameter is delivered once per step, between ``begin_step`` and
+        ``finish_step``: a second delivery (gradient accumulation without
+        ``no_sync``, a backward outside the step) would relaunch its bucket
+        against barrier slots its peers already passed, so it raises."""
+        if not self._in_step:
+            raise InfeasibleConfigError(
+                f"grad_ready({param_index}) outside begin_step/finish_step (wrap accumulation "
+                "micro-batches in no_sync())")
         slot = self.layout.slot(param_index)
+        if self._launched[slot.bucket]:
+            raise InfeasibleConfigError(
+                f"gradient of param {param_index} delivered again after bucket {slot.bucket} was launched")
         pend = self._pending_grads[slot.bucket]
+        if param_index in pend:
+            raise InfeasibleConfigError(f"gradient of param {param_index} delivered twice in one step")
         pend[param_index] = grad
         b = self.layout.buckets[slot.bucket]
         if len(pend) == len(b.slots):
@@ -387,8 +440,17 @@ class DistributedOptimizer:
         else:
             self._ev_end.record(self.s_comm if self.backend in ("p2p", "nvls") else self.s_opt)
         self._in_step = False
+        if self.backend in ("p2p", "nvls"):
+            # asynchronous read-back of the error word (checked at the next
+            # begin_step once it has landed; StepReport.resolve checks it too)
+            s = self.s_comm
+            with torch.cuda.stream(s):
+                self._err_host.copy_(self._err, non_blocking=True)
+            self._ev_err.record(s)
+            self._err_pending = True
         rep = StepReport(self.step_count, len(L.buckets), L.total_numel // self.dp,
-                         start=self._ev_start, end=self._ev_end)
+                         start=self._ev_start, end=self._ev_end,
+                         err=self._err if self.backend in ("p2p", "nvls") else None)
         if self.clip is not None:
             rep.grad_norm, rep.clip_coef = self._norm, self._coef
         return rep
@@ -449,6 +511,38 @@ class DistributedOptimizer:
         self.s_h2d = torch.cuda.Stream(device=self.device)
         self._ev_h2d = [torch.cuda.Event() for _ in self.layout.buckets]
 
+    def gather_params(self) -> None:
+        """All-gather every bucket's bf16 param shard from its owner into
+        every rank's param buffer (after ``checkpoint.load`` restored only the
+        local shards).  p2p/nvls: copy-engine stores of the own shard into each
+        peer's buffer, then an end-of-step barrier; nccl: AllGather per
+        bucket.  Stream-ordered, no host synchronisation; every rank calls it."""
+        if self._in_step:
+            raise InfeasibleConfigError("gather_params inside a step")
+        cur = torch.cuda.current_stream(self.device)
+        s = self.s_comm
+        s.wait_stream(cur)
+        L = self.layout
+        if self.backend == "nccl":
+            for b in L.buckets:
+                lo, hi = b.shard_range(self.shard_index, self.dp)
+                self.comm.all_gather_bf16(_ptr(self.param_buffer) + 2 * lo, _ptr(self.param_buffer) + 2 * b.start,
+                                          hi - lo, s)
+        elif self.backend in ("p2p", "nvls"):
+            for b in L.buckets:
+                lo, hi = b.shard_range(self.shard_index, self.dp)
+                for q in range(self.dp):
+                    if q != self.shard_index:
+                        nat.call("hod_ce_copy", self._sym_param.peer(q, 2 * lo), _ptr(self.param_buffer) + 2 * lo,
+                                 2 * (hi - lo), nat.stream_ptr(s))
+            self._epoch += 1
+            nb = len(L.buckets)
+            nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,
+                     self._epoch, nb, self.timeout_ns, _ptr(self._err), nat.stream_ptr(s))
+        for ev in self._ev_params:
+            ev.record(s)
+        cur.wait_stream(s)
+
     def wait_params(self, bucket: int, stream=None) -> None:
         """Make ``stream`` (default: current) wait until bucket's params are gathered."""
         (stream or torch.cuda.current_stream(self.device)).wait_event(self._ev_params[bucket])
@@ -456,15 +550,40 @@ class DistributedOptimizer:
     def register_hooks(self, module_params) -> list:
         """Attach post-accumulate-grad hooks: parameter i's gradient feeds
         ``grad_ready(i)``.  ``module_params[i]`` must be the model parameter
-        for registration index i."""
+        for registration index i.  Backward passes of accumulation
+        micro-batches run under ``no_sync()`` (the hooks stay silent and the
+        gradients accumulate in ``p.grad``); the last micro-batch's backward,
+        inside ``begin_step``/``finish_step``, delivers the sums."""
         if self._pre_barrier_auto:
             self.pre_barrier = True
         handles = []
         for i, p in enumerate(module_params):
             def hook(param, i=i):
-                self.grad_ready(i, param.grad)
+                if self._sync_enabled:
+                    self.grad_ready(i, param.grad)
             handles.append(p.register_post_accumulate_grad_hook(hook))
         return handles
+
+    def no_sync(self):
+        """Context manager: hooks registered by ``register_hooks`` do not
+        deliver gradients inside it (gradient-accumulation micro-batches)."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def ctx():
+            prev, self._sync_enabled = self._sync_enabled, False
+            try:
+                yield
+            finally:
+                self._sync_enabled = prev
+        return ctx()
+
+    def poll_error(self) -> None:
+        """Raise DeviceError if an earlier step's read-back error word is
+        nonzero.  Never blocks: a read-back still in flight is checked later."""
+        if self._err_pending and self._ev_err.query():
+            self._err_pending = False
+            raise_device_error(int(self._err_host[0]))
 
     def close(self) -> None:
         for c in {id(x): x for x in (self.comm, self.norm_comm) if x is not None}.values():
@@ -483,11 +602,15 @@ class DistributedOptimizer:
 
     def _launch_bucket(self, bi: int) -> None:
         last = sum(self._launched) == len(self._launched) - 1
-        nat.call("hod_set_grid_limit", 0 if (last or not self.sm_budget) else int(self.sm_budget))
+        base = nat.grid_base()
+        if last or not self.sm_budget:
+            self._launch_bucket_body(bi)
+            return
+        nat.call("hod_set_grid_limit", min(int(self.sm_budget), base) if base else int(self.sm_budget))
         try:
             self._launch_bucket_body(bi)
         finally:
-            nat.call("hod_set_grid_limit", 0)
+            nat.call("hod_set_grid_limit", base)
 
     def _launch_bucket_body(self, bi: int) -> None:
         b = self.layout.buckets[bi]
@@ -519,8 +642,7 @@ class DistributedOptimizer:
             entries[k].dst_offset = s.offset
         bucket_ptr = _ptr(self.grad_buffer) + 2 * b.start
         src_bytes = 4 if dtype == nat.HOD_DTYPE_F32 else 2
-        if self.backend == "none" and not self.keep_reduced and (
-                self.clip is None or len(b.slots) <= nat.HOD_PACK_MAX_ENTRIES):
+        if self.backend == "none" and not self.keep_reduced:
             # d == 1: nothing to exchange, so K1 and K2 fuse (no bucket round
             # trip).  With clipping the norm needs every bucket first: a
             # 2 B/element norm pass now, the fused update after the norm.
@@ -536,17 +658,10 @@ class DistributedOptimizer:
             self._deferred_pa.append((bi, entries, dtype))
             return
         chained = self._grads_resident   # back-to-back launches: timed as one PDL run
-        push = self.backend == "p2p" and self.rs_push
-        t0 = self._timed_event(self.s_pack, run=("pack_push" if push else "pack") if chained else None)
-        if push:
-            dsts = (ctypes.c_void_p * self.dp)(*[self._sym_grad.peer(q) + 2 * b.start for q in range(self.dp)])
-            nat.call("hod_pack_push", entries, len(b.slots), b.numel, ctypes.c_float(self.grad_scale), dtype,
-                     dsts, self.dp, self.shard_index, nat.stream_ptr(self.s_pack))
-            self._timed_close("pack_push", t0, self.s_pack, (src_bytes + 2) * b.numel)
-        else:
-            nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
-                     ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
-            self._timed_close("pack", t0, self.s_pack, (src_bytes + 2) * b.numel)
+        t0 = self._timed_event(self.s_pack, run="pack" if chained else None)
+        nat.call("hod_pack_bf16", entries, len(b.slots), bucket_ptr, b.numel,
+                 ctypes.c_float(self.grad_scale), dtype, nat.stream_ptr(self.s_pack))
+        self._timed_close("pack", t0, self.s_pack, (src_bytes + 2) * b.numel)
         self._ev_packed[bi].record(self.s_pack)
         self._launched[bi] = True
 
@@ -655,8 +770,8 @@ class DistributedOptimizer:
         sp.n_buckets = len(bis)
         sp.d, sp.rank, sp.nvls = d, self.shard_index, int(self.backend == "nvls")
         sp.keep_reduced = int(self.keep_reduced)
-        sp.slot, sp.epoch, sp.timeout_ns = bis[0], self.step_count, self.timeout_ns
-        sp.staged = int(self.backend == "p2p" and self.rs_push)
+        sp.slot, sp.epoch, sp.timeout_ns = bis[0], self._epoch, self.timeout_ns
+        sp.tag = nat.span_tag(bis[0], bis[-1])
         hp = self._hp()
         name = {nat.HOD_P2P_FUSED: "fused", nat.HOD_P2P_RS: "rs", nat.HOD_P2P_ADAMW_AG: "adamw_ag"}[mode]
         # algorithmic bytes per launch: local HBM (state 24 B + own param 2 B +
@@ -664,7 +779,7 @@ class DistributedOptimizer:
         nbytes = {"fused": 28 * n_total, "rs": 2 * d * n_total + 2 * n_total, "adamw_ag": 28 * n_total}[name]
         if self.pre_barrier and mode != nat.HOD_P2P_ADAMW_AG:
             nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), d, self.shard_index, sp.slot,
-                     sp.epoch, self.timeout_ns, _ptr(self._err), nat.stream_ptr(self.s_comm))
+                     sp.epoch, sp.tag, self.timeout_ns, _ptr(self._err), nat.stream_ptr(self.s_comm))
         t0 = self._timed_event(self.s_comm)
         nat.call("hod_p2p_step", ctypes.byref(sp), mode, ctypes.byref(hp), nat.stream_ptr(self.s_comm))
         self._timed_close(name, t0, self.s_comm, nbytes)
@@ -720,7 +835,7 @@ class DistributedOptimizer:
                 xchg = self._flag_ptrs(self._norm_xchg)
                 flags = self._flag_ptrs(self._norm_flags)
                 nat.call("hod_p2p_norm", _ptr(self._partials), nb * nat.HOD_SUMSQ_PARTIALS, xchg, flags,
-                         self._norm_d, self._norm_rank, 0, self.step_count, self.timeout_ns,
+                         self._norm_d, self._norm_rank, 0, self._epoch, self.timeout_ns,
                          _ptr(self._err), ctypes.c_float(self.clip), _ptr(self._coef), _ptr(self._norm),
                          _ptr(self._sumsq), nat.stream_ptr(s))
             # reverse bucket order: the last bucket holds the first layers, which
@@ -734,7 +849,7 @@ class DistributedOptimizer:
             # end-of-step barrier: every rank's param stores (and reads of our
             # buckets) are complete before anyone uses the params or repacks
             nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index, nb,
-                     self.step_count, self.timeout_ns, _ptr(self._err), nat.stream_ptr(s))
+                     self._epoch, nb, self.timeout_ns, _ptr(self._err), nat.stream_ptr(s))
             for ev in self._ev_params:
                 ev.record(s)
 
@@ -746,19 +861,15 @@ class DistributedOptimizer:
             return
         nb = len(self.layout.buckets)
         nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), self.dp, self.shard_index,
-                 nb + 1 + span[0], self.step_count, self.timeout_ns, _ptr(self._err),
-                 nat.stream_ptr(self.s_comm))
+                 nb + 1 + span[0], self._epoch, nat.span_tag(span[0], span[-1]), self.timeout_ns,
+                 _ptr(self._err), nat.stream_ptr(self.s_comm))
         for b in span:
             self._ev_params[b].record(self.s_comm)
 
     def check_health(self) -> None:
-        """Raise DeviceError if a cross-GPU barrier timed out (synchronises)."""
-        if getattr(self, "_err", None) is not None:
-            code = int(self._err.item())
-            if code:
-                from .errors import DeviceError
-
-                raise DeviceError(f"fused collective reported error {code} (barrier timeout)")
+        """Raise DeviceError if a cross-GPU barrier timed out or met a
+        mismatched span (synchronises)."""
+        raise_device_error(int(self._err.item()))
 
     def _norm_then_pack_adamw(self) -> None:
         """d == 1 with clipping: every bucket's norm partials exist; finish the

@@ -54,10 +54,9 @@ def main():
     gs = config_gradset(a.config)
     gdt = torch.float32 if a.grad_dtype == "f32" else torch.bfloat16
     clip = a.clip if a.clip > 0 else None
-    backend, push = (a.backend[:-5], True) if a.backend.endswith("-push") else (a.backend, False)
     opt = DistributedOptimizer(init_params(gs, dev), bucket_size=a.bucket, clip=clip,
-                               dp_group=DPGroup(tuple(range(world)), rank), backend=backend,
-                               keep_reduced=True, barrier_timeout_s=30.0, rs_push=push)
+                               dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
+                               keep_reduced=True, barrier_timeout_s=30.0)
     L = opt.layout
     out = Path(a.out)
     for step in range(1, a.steps + 1):

@@ -31,29 +31,15 @@ def u16(t):
 
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("clip", [None, 0.02])
-@pytest.mark.parametrize("push", [False, True])
-def test_emulated_d_way_fused_step(oracle, native, d, clip, push):
-    """push=True: every rank's bucket is scattered by hod_pack_push into the
-    owners' slots first, then the kernel reduces the d slots locally (staged);
-    same bits as the pull."""
+def test_emulated_d_way_fused_step(oracle, native, d, clip):
     gs = odd_tensors()
     L = build_bucket_layout(gs.numels, 200_000, dp=d)
     total, nb = L.total_numel, len(L.buckets)
     gen = torch.Generator(device=DEV).manual_seed(100 + d)
     packs = [torch.randn(total, generator=gen, device=DEV).mul_(1e-3).to(torch.bfloat16) for _ in range(d)]
-    if push:
-        grads = [torch.full_like(p, 3.0) for p in packs]  # garbage: every slot gets pushed
-        for b in L.buckets:
-            dsts = (ctypes.c_void_p * d)(*[g.data_ptr() + 2 * b.start for g in grads])
-            for r in range(d):
-                e = (nat.PackEntry * 1)()
-                e[0].src, e[0].numel, e[0].dst_offset = packs[r].data_ptr() + 2 * b.start, b.numel, 0
-                nat.call("hod_pack_push", e, 1, b.numel, ctypes.c_float(1.0), nat.HOD_DTYPE_BF16,
-                         dsts, d, r, 0)
-    else:
-        grads = [p.clone() for p in packs]      # per-rank grad buffers (RS writes in place)
+    grads = [p.clone() for p in packs]      # per-rank grad buffers (RS writes in place)
     params = [torch.zeros(total, dtype=torch.bfloat16, device=DEV) for _ in range(d)]
-    flags = [torch.zeros((2 * nb + 1) * 8, dtype=torch.int32, device=DEV) for _ in range(d)]
+    flags = [torch.zeros((2 * nb + 1) * 8, dtype=torch.int64, device=DEV) for _ in range(d)]
     shard_total = total // d
     state = [[torch.randn(shard_total, generator=gen, device=DEV).mul_(0.02),
               torch.rand(shard_total, generator=gen, device=DEV).mul_(1e-3),
@@ -80,12 +66,13 @@ def test_emulated_d_way_fused_step(oracle, native, d, clip, push):
             sp.bucket_start[k], sp.shard_numel[k] = L.buckets[bi].start, L.buckets[bi].numel // d
         sp.n_buckets, sp.d, sp.rank, sp.nvls, sp.keep_reduced = len(span), d, r, 0, 1
         sp.slot, sp.epoch, sp.timeout_ns = span[0], 1, 5_000_000_000
-        sp.staged = int(push)
+        sp.tag = nat.span_tag(span[0], span[-1])
         return sp
 
     def arrive_all(slot):
         for q in range(d):
-            flags[q].view(-1, 8)[slot, :d] = 1   # every peer has signalled epoch 1
+            tag = nat.span_tag(slot, next(sp_[-1] for sp_ in spans if sp_[0] == slot))
+            flags[q].view(-1, 8)[slot, :d] = (1 << 32) | tag   # every peer has signalled epoch 1
 
     if clip is None:
         for span in spans:
@@ -126,37 +113,3 @@ def test_emulated_d_way_fused_step(oracle, native, d, clip, push):
             np.testing.assert_array_equal(full[b.start + r * n:b.start + (r + 1) * n], want)
             dev_master = state[r][0][offs[bi]:offs[bi] + n].cpu().numpy()
             np.testing.assert_array_equal(dev_master.view(np.uint32), master.view(np.uint32))
-
-
-@pytest.mark.parametrize("d", [2, 3, 4, 8])
-@pytest.mark.parametrize("src_dtype", [torch.bfloat16, torch.float32])
-def test_pack_push_slots_match_oracle_pack(oracle, native, d, src_dtype):
-    """hod_pack_push from real (odd-size, gapped) tensor tables: slot r of rank
-    q's bucket region == shard q of the oracle's pack of rank r's gradients."""
-    gs = odd_tensors()
-    L = build_bucket_layout(gs.numels, 150_000, dp=d)
-    gen = torch.Generator(device=DEV).manual_seed(7 + d)
-    per_rank = [[torch.randn(t.shape, generator=gen, device=DEV).mul_(1e-2).to(src_dtype) for t in gs.tensors]
-                for _ in range(d)]
-    bufs = [torch.full((L.total_numel,), 5.0, dtype=torch.bfloat16, device=DEV) for _ in range(d)]
-    scale = 1.0 / 3.0
-    dt = nat.HOD_DTYPE_F32 if src_dtype == torch.float32 else nat.HOD_DTYPE_BF16
-    for b in L.buckets:
-        dsts = (ctypes.c_void_p * d)(*[x.data_ptr() + 2 * b.start for x in bufs])
-        for r in range(d):
-            gl = [per_rank[r][s_.index].reshape(-1) for s_ in b.slots]
-            e = (nat.PackEntry * len(gl))()
-            for k, (g, s_) in enumerate(zip(gl, b.slots)):
-                e[k].src, e[k].numel, e[k].dst_offset = g.data_ptr(), g.numel(), s_.offset
-            nat.call("hod_pack_push", e, len(gl), b.numel, ctypes.c_float(scale), dt, dsts, d, r, 0)
-    torch.cuda.synchronize()
-    host = [u16(x) for x in bufs]
-    for b in L.buckets:
-        n = b.numel // d
-        for r in range(d):
-            gl = [per_rank[r][s_.index].reshape(-1) for s_ in b.slots]
-            cpu = [g.cpu().numpy() if src_dtype == torch.float32 else u16(g) for g in gl]
-            want = oracle.pack(cpu, [s_.offset for s_ in b.slots], b.numel, scale)
-            for q in range(d):
-                got = host[q][b.start + r * n:b.start + (r + 1) * n]
-                np.testing.assert_array_equal(got, want[q * n:(q + 1) * n])

@@ -115,8 +115,6 @@ CASES = [
     (8, "toy", "bf16", 2_000_000, 0.0, "p2p"),
     (8, "toy", "bf16", 2_000_000, 1.0, "nvls"),
     (8, "toy", "bf16", 2_000_000, 0.0, "nccl"),
-    (2, "odd", "bf16", 300_000, 0.05, "p2p-push"),  # RS pushed by the pack (hod_pack_push)
-    (4, "toy", "f32", 3_000_000, 0.0, "p2p-push"),
 ]
 
 

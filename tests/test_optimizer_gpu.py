@@ -150,3 +150,99 @@ def test_empty_parameter_list_is_rejected(native):
 
     with pytest.raises(InfeasibleConfigError):
         DistributedOptimizer([])
+
+
+@pytest.mark.parametrize("clip", [0.01, None])
+def test_long_pack_table_bucket_beside_short_one(oracle, native, clip):
+    """d = 1: one bucket holding 71 tensors (> HOD_PACK_MAX_ENTRIES, windowed
+    norm pass and update) next to a 1-tensor bucket.  Round 1 sent the long
+    bucket down a route that never updated it when clipping deferred the
+    short one; every bucket must match the oracle."""
+    shapes = [(50_000,), (100_000,)] + [(257,)] * 70
+    g = torch.Generator(device="cpu").manual_seed(11)
+    p0 = [(torch.randn(s, generator=g) * 0.02).to(DEV) for s in shapes]
+    opt = DistributedOptimizer(p0, bucket_size=30_000, clip=clip)
+    L = opt.layout
+    assert [len(b.slots) for b in L.buckets] == [71, 1]
+    state = _oracle_state(oracle, L, [p.cpu().numpy() for p in p0])
+    for step in (1, 2, 3):
+        grads = [(torch.randn(s, generator=g) * 1e-3).to(torch.bfloat16).to(DEV) for s in shapes]
+        rep = opt.step(grads)
+        torch.cuda.synchronize()
+        params, norm = oracle.step_all_ranks([[u16(x) for x in grads]], [
+            {"params": [(s.index, s.offset, s.numel) for s in b.slots], "numel": b.numel}
+            for b in L.buckets], state, step, opt.lr, opt.betas, opt.eps, opt.weight_decay, clip=clip)
+        if clip is not None:
+            assert abs(rep.resolve()["grad_norm"] - norm) <= 1e-5 * norm
+        pb = u16(opt.param_buffer)
+        for bi, b in enumerate(L.buckets):
+            master = state[bi][0][0]
+            off = L.shard_offsets()[bi]
+            dev_master = opt.master[off:off + b.numel].cpu().numpy()
+            if clip is None:
+                np.testing.assert_array_equal(pb[b.start:b.start + b.numel], params[bi])
+                np.testing.assert_array_equal(dev_master, master)
+            else:
+                np.testing.assert_allclose(dev_master, master, rtol=1e-6, atol=1e-6 * np.abs(master).max())
+                assert not np.array_equal(dev_master, p0_master(p0, b)), f"bucket {bi} never updated"
+    opt.close()
+
+
+def p0_master(p0, b):
+    flat = np.zeros(b.numel, np.float32)
+    for s in b.slots:
+        flat[s.offset:s.offset + s.numel] = p0[s.index].cpu().numpy().reshape(-1)
+    return flat
+
+
+def test_grad_delivery_errors_and_no_sync(native):
+    """grad_ready outside a step, twice for one param, or after its bucket
+    launched raises; no_sync() silences the hooks for accumulation
+    micro-batches and the last backward delivers the accumulated sum."""
+    from paper_2312_03549_b200.errors import InfeasibleConfigError
+
+    gs = config_gradset("odd")
+    p0 = init_params(gs, DEV)
+    opt = DistributedOptimizer(p0, bucket_size=100_000)
+    g = make_grads(gs, 1, 0, DEV)
+    with pytest.raises(InfeasibleConfigError):
+        opt.grad_ready(0, g[0])
+    opt.begin_step()
+    last = len(g) - 1
+    opt.grad_ready(last, g[last])
+    b = opt.layout.slot(last).bucket
+    if len(opt.layout.buckets[b].slots) > 1:
+        with pytest.raises(InfeasibleConfigError):
+            opt.grad_ready(last, g[last])
+    for s in opt.layout.buckets[b].slots:
+        if s.index != last:
+            opt.grad_ready(s.index, g[s.index])
+    with pytest.raises(InfeasibleConfigError):   # bucket b already launched
+        opt.grad_ready(last, g[last])
+    for i in range(len(g)):
+        if opt.layout.slot(i).bucket != b:
+            opt.grad_ready(i, g[i])
+    opt.finish_step()
+    opt.close()
+
+    # accumulation: two micro-batches under no_sync + one delivering == one
+    # step on the sum of the three
+    params = [torch.nn.Parameter(p.clone()) for p in p0]
+    ref = DistributedOptimizer(p0, bucket_size=100_000)
+    acc = DistributedOptimizer(p0, bucket_size=100_000)
+    acc.register_hooks(params)
+    micro = [make_grads(gs, k, 0, DEV, dtype=torch.float32) for k in (1, 2, 3)]
+    for k, mg in enumerate(micro):
+        loss = sum((p * x).sum() for p, x in zip(params, mg))
+        if k < 2:
+            with acc.no_sync():
+                loss.backward()
+        else:
+            acc.begin_step()
+            loss.backward()
+            acc.finish_step()
+    ref.step([p.grad.clone() for p in params])
+    torch.cuda.synchronize()
+    assert torch.equal(acc.param_buffer, ref.param_buffer)
+    ref.close()
+    acc.close()

@@ -1,6 +1,6 @@
 """The fused span kernel of ONE rank on ONE GPU (peers emulated; for ncu).
 
-    python tools/fused_emulated.py [--d 2] [--numel 268435456] [--mode fused|rs|adamw_ag] [--staged]
+    python tools/fused_emulated.py [--d 2] [--numel 268435456] [--mode fused|rs|adamw_ag]
 
 All d ranks' buffers live on this device and every barrier flag is pre-set,
 so the launch runs straight through with the exact d-way code path (peer
@@ -27,7 +27,6 @@ def main():
     ap.add_argument("--d", type=int, default=2)
     ap.add_argument("--numel", type=int, default=1 << 28)
     ap.add_argument("--mode", default="fused", choices=["fused", "rs", "adamw_ag"])
-    ap.add_argument("--staged", action="store_true")
     ap.add_argument("--iters", type=int, default=10)
     a = ap.parse_args()
     nat.load()
@@ -36,7 +35,7 @@ def main():
     n = N // d
     grads = [torch.randn(N, device=dev).mul_(1e-3).to(torch.bfloat16) for _ in range(d)]
     params = [torch.zeros(N, dtype=torch.bfloat16, device=dev) for _ in range(d)]
-    flags = [torch.ones(8 * 8, dtype=torch.int32, device=dev) for _ in range(d)]
+    flags = [torch.full((8 * 8,), 1 << 32, dtype=torch.int64, device=dev) for _ in range(d)]
     st = [torch.randn(n, device=dev) * 0.02, torch.zeros(n, device=dev), torch.zeros(n, device=dev)]
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     parts = torch.zeros(nat.HOD_SUMSQ_PARTIALS, device=dev)
@@ -51,7 +50,6 @@ def main():
     sp.bucket_start[0], sp.shard_numel[0] = 0, n
     sp.n_buckets, sp.d, sp.rank, sp.nvls, sp.keep_reduced = 1, d, 0, 0, 0
     sp.slot, sp.epoch, sp.timeout_ns = 0, 1, 5_000_000_000
-    sp.staged = int(a.staged)
     mode = {"fused": nat.HOD_P2P_FUSED, "rs": nat.HOD_P2P_RS, "adamw_ag": nat.HOD_P2P_ADAMW_AG}[a.mode]
     if mode == nat.HOD_P2P_RS:
         sp.partials = parts.data_ptr()
@@ -74,7 +72,7 @@ def main():
     ms = e0.elapsed_time(e1) / a.iters
     # local HBM bytes per owned element: d grad reads + (fused/adamw_ag) 24 B state + d param writes
     per = {"fused": 2 * d + 24 + 2 * d, "rs": 2 * d + 2, "adamw_ag": 2 + 24 + 2 * d}[a.mode]
-    print(json.dumps({"d": d, "mode": a.mode, "staged": a.staged, "owned_elems": n, "ms": round(ms, 4),
+    print(json.dumps({"d": d, "mode": a.mode, "owned_elems": n, "ms": round(ms, 4),
                       "Gelem_per_s": round(n / ms / 1e6, 1), "bytes_per_owned_elem": per,
                       "hbm_GBps": round(per * n / ms / 1e6, 1)}))
 

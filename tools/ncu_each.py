@@ -4,7 +4,7 @@
         -o gpurun_out/prof_each python tools/ncu_each.py
 
 One GPU.  Kernels whose peers live on other GPUs (the fused span kernel in
-FUSED / RS / ADAMW_AG modes, pack_push) run with all d ranks' buffers on this
+FUSED / RS / ADAMW_AG modes) run with all d ranks' buffers on this
 device and every barrier flag pre-set — the exact d-way code path with peer
 loads/stores turned into local ones (tools/fused_emulated.py) — so their DRAM
 traffic includes what the peers' NVLink traffic would put on HBM.  Prints the
@@ -36,12 +36,12 @@ def entries(srcs):
     return e
 
 
-def span_kernel(d, mode, staged=False, n_bucket=NB * 4):
+def span_kernel(d, mode, n_bucket=NB * 4):
     """One emulated rank-0 launch of p2p_step_kernel over one bucket."""
     n = n_bucket // d
     grads = [torch.randn(n_bucket, device=DEV).mul_(1e-3).to(torch.bfloat16) for _ in range(d)]
     params = [torch.zeros(n_bucket, dtype=torch.bfloat16, device=DEV) for _ in range(d)]
-    flags = [torch.ones(8 * 8, dtype=torch.int32, device=DEV) for _ in range(d)]
+    flags = [torch.full((8 * 8,), 1 << 32, dtype=torch.int64, device=DEV) for _ in range(d)]
     st = [torch.randn(n, device=DEV) * 0.02, torch.zeros(n, device=DEV), torch.zeros(n, device=DEV)]
     err = torch.zeros(1, dtype=torch.int32, device=DEV)
     parts = torch.zeros(nat.HOD_SUMSQ_PARTIALS, device=DEV)
@@ -55,7 +55,6 @@ def span_kernel(d, mode, staged=False, n_bucket=NB * 4):
     sp.bucket_start[0], sp.shard_numel[0] = 0, n
     sp.n_buckets, sp.d, sp.rank, sp.nvls, sp.keep_reduced = 1, d, 0, 0, 0
     sp.slot, sp.epoch, sp.timeout_ns = 0, 1, 5_000_000_000
-    sp.staged = int(staged)
     m = {"fused": nat.HOD_P2P_FUSED, "rs": nat.HOD_P2P_RS, "adamw_ag": nat.HOD_P2P_ADAMW_AG}[mode]
     if m == nat.HOD_P2P_RS:
         sp.partials = parts.data_ptr()

@@ -24,7 +24,7 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent.parent
 OURS = re.compile(r"hod::|pack_kernel|adamw_vec_kernel|adamw_scalar_kernel|sumsq_kernel|p2p_step_kernel|"
                   r"barrier_kernel|norm_exchange_kernel|sum_partials_kernel|clip_coef_kernel|pack_adamw|pack_sumsq|"
-                  r"pack_push|accumulate_partials")
+                  r"accumulate_partials")
 
 
 def short(name: str) -> str:

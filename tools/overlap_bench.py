@@ -173,7 +173,7 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, sm_budget: int = 
     flops = sum(4 * T * t.shape[0] * t.shape[1] for t in gs.tensors if len(t.shape) == 2
                 and "embed" not in t.name)
     doc = {"world": world, "backend": opt.backend, "tokens_per_gpu": T,
-           "pre_barrier": opt.pre_barrier, "rs_push": opt.rs_push, "span_numel": opt.span_numel,
+           "pre_barrier": opt.pre_barrier, "span_numel": opt.span_numel,
            "sm_budget": sm_budget,
            "clip": opt.clip, "buckets": len(opt.layout.buckets),
            "t_backward_ms": round(t_bwd, 3), "t_backward_carved_ms": round(t_bwd_carved, 3),
@@ -209,7 +209,6 @@ def main():
                          "same number of SMs carved out (torch._C._set_sm_carveout_experimental)")
     ap.add_argument("--pre-barrier", type=int, default=None,
                     help="1: arrival barrier as a 1-CTA kernel before each span (optimizer pre_barrier)")
-    ap.add_argument("--rs-push", type=int, default=None, help="1: reduce-scatter by push (hod_pack_push)")
     ap.add_argument("--span-numel", type=int, default=None, help="fused-launch span threshold (elements)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -225,7 +224,6 @@ def main():
                                dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
                                sm_budget=a.sm_budget or None,
                                pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier),
-                               rs_push=None if a.rs_push is None else bool(a.rs_push),
                                **({"span_numel": a.span_numel} if a.span_numel else {}))
     del p0
     doc = measure(opt, gs, a.tokens, a.iters, world, dev, sm_budget=a.sm_budget)

@@ -59,7 +59,7 @@ def measure_bucket(numel, iters, world, rank, dev, comm, cases=None) -> dict:
     pg = dist.group.WORLD
     g = SymmetricTensor(N, torch.bfloat16, dev, pg)
     p = SymmetricTensor(N, torch.bfloat16, dev, pg, zero=True)
-    fl = SymmetricTensor(64 * 8, torch.int32, dev, pg, zero=True)
+    fl = SymmetricTensor(64 * 8, torch.int64, dev, pg, zero=True)
     g.tensor.normal_(0, 1e-3)
     master = torch.randn(n, device=dev) * 0.02
     m = torch.zeros(n, device=dev)
