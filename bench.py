@@ -41,7 +41,8 @@ CONFIGS = {
 }
 FALLBACK_HBM_GBS = 6650.0
 NVLINK_MEASURED = 770.0   # GB/s per direction per GPU, peer copy (B200_PROFILING.md)
-NVLINK_NOMINAL = 900.0    # NVLink 5, 18 links
+NVLINK_NOMINAL = 900.0    # NVLink 5, 18 links: the north star's and SURVEY §8d's denominator
+NVLINK_PEAK = NVLINK_NOMINAL   # headline roofline denominator; the measured copy is reported beside it
 
 KERNEL_NAMES = {
     "adamw": "hod adamw_vec_kernel (K2)",
@@ -58,6 +59,19 @@ def _desc(cfg, clip) -> str:
     """Workload text with the clip actually used (``--clip`` may override it)."""
     base = cfg["desc"].replace(", grad-norm clip 1.0", "")
     return base + (f", grad-norm clip {clip}" if clip else ", no clip")
+
+
+def _config_doc(args, clip, params, buckets, dp, scen=None) -> dict:
+    """The ``config`` object of the JSON line — identical for both arms (the
+    driver compares them); implementation details live outside it."""
+    cfg = CONFIGS[args.config]
+    hbm_gb = {"gpt1.3b": 37, "llama7b": 190, "toy": 0.5}.get(args.config, 0)
+    return {"workload": (f"scenario {scen['scenario']}: GPT stages {scen['stage_layers']} "
+                         "(reference self-adapting partition), PP x DP, world clip norm"
+                         if scen else _desc(cfg, clip)),
+            "config": "scenario" if scen else args.config, "params": params,
+            "scenario": scen, "buckets": buckets, "bucket_size": args.bucket_size, "dp": dp, "clip": clip,
+            "l2": f"inputs (~{hbm_gb} GB per step) >> 126 MB L2, no flush needed"}
 
 
 def _peaks():
@@ -199,6 +213,122 @@ def _emulated_traffic_ratio(dom: str, d: int, backend: str):
     return None
 
 
+def parity_probe(opt, gs, rank: int, dev, gdtype, world: int) -> dict:
+    """Self-check AFTER the timed region (the line then carries its own
+    correctness): one more step of the benchmarked optimizer over
+    the same gradients, then the first, middle and last bucket of this rank
+    against the oracle (oracle/oracle.py — the checker, never the measured
+    path): every DP peer's gradients are regenerated from their seeds,
+    packed and reduce-scattered by the oracle (rank-order fp32 sum of
+    simulator.py:81-89 semantics over the DP row of groups.py:137-148;
+    NVLS / NCCL within d/2 bf16 ulp of sum|x|), then the oracle AdamW from
+    the pre-step state with the device's reduced shard and clip coefficient
+    must give master / m / v / the gathered bf16 params bit-exactly; the
+    clip coefficient must be bit-identical on every rank.  ``ok`` is the AND
+    over all ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle
+    from paper_2312_03549_b200.errors import DeviceError
+    from paper_2312_03549_b200.synthetic import make_grads
+
+    def u16(t):
+        return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+    t0 = time.perf_counter()
+    oracle.set_threads(max(1, len(os.sched_getaffinity(0)) // max(1, torch.cuda.device_count())))
+    L = opt.layout
+    nb = len(L.buckets)
+    sample = sorted({0, nb // 2, nb - 1})
+    offs = L.shard_offsets()
+    d, me = opt.dp, opt.shard_index
+    out = {"buckets_checked": sample, "dp": d, "backend": opt.backend, "ok": False}
+    errors = []
+    pre = {}
+    for bi in sample:
+        n = L.buckets[bi].numel // d
+        pre[bi] = tuple(x[offs[bi]:offs[bi] + n].cpu().numpy().copy() for x in (opt.master, opt.exp_avg, opt.exp_avg_sq))
+    keep = opt.keep_reduced
+    opt.keep_reduced = d > 1                 # leave the reduced shard in place for the check
+    grads = None
+    try:
+        grads = make_grads(gs, 1, opt.group.global_rank, dev, dtype=gdtype)
+        rep = opt.step(grads)
+        rep.resolve()
+    except DeviceError as e:
+        errors.append(f"device: {e}")
+        rep = None
+    finally:
+        opt.keep_reduced = keep
+    del grads
+    torch.cuda.empty_cache()
+    coef = None
+    if rep is not None and rep.clip_coef is not None:
+        c = rep.clip_coef.reshape(1).clone()
+        if world > 1:
+            cs = [torch.zeros_like(c) for _ in range(world)]
+            dist.all_gather(cs, c)
+            if any(not torch.equal(x.view(torch.int32), c.view(torch.int32)) for x in cs):
+                errors.append("clip coefficient differs between ranks")
+        coef = float(c.item())
+    if rep is not None:
+        slices = {bi: [] for bi in sample}
+        for q in opt.group.ranks:
+            gq = make_grads(gs, 1, q, dev, dtype=gdtype)
+            for bi in sample:
+                b = L.buckets[bi]
+                srcs = [(u16(gq[s.index]) if gdtype == torch.bfloat16 else gq[s.index].cpu().numpy()).reshape(-1)
+                        for s in b.slots]
+                full = oracle.pack(srcs, [s.offset for s in b.slots], b.numel, opt.grad_scale)
+                sh = b.numel // d
+                slices[bi].append(full[me * sh:(me + 1) * sh].copy())
+                del full, srcs
+            del gq
+            torch.cuda.empty_cache()
+        exact = opt.backend in ("p2p", "none")
+        out["reduce_scatter_rule"] = ("bit-exact rank-order fp32 sum" if exact
+                                      else "within d/2 bf16 ulp of sum|x| (switch / ring order)")
+        step = opt.step_count
+        checked = 0
+        for bi in sample:
+            b = L.buckets[bi]
+            lo, hi = b.shard_range(me, d)
+            if d > 1:
+                dev_red = u16(opt.grad_buffer[lo:hi])
+                if exact:
+                    if not np.array_equal(dev_red, oracle.sum_slices(slices[bi])):
+                        errors.append(f"bucket {bi}: reduced shard")
+                else:
+                    f64 = oracle.sum_slices_f64(slices[bi])
+                    absum = sum(np.abs(oracle.bf16_to_f32(x).astype(np.float64)) for x in slices[bi])
+                    err = np.abs(oracle.bf16_to_f32(dev_red).astype(np.float64) - f64)
+                    ulp = np.exp2(np.floor(np.log2(np.maximum(absum, np.finfo(np.float32).tiny))) - 7)
+                    if not np.all(err <= d * 0.5 * ulp + 1e-30):
+                        errors.append(f"bucket {bi}: reduced shard outside the bf16 bound")
+            else:
+                dev_red = slices[bi][0]
+            master, m, v = (x.copy() for x in pre[bi])
+            want_p = oracle.adamw(master, m, v, dev_red, step, opt.lr, opt.betas, opt.eps, opt.weight_decay,
+                                  coef=coef)
+            o, n = offs[bi], hi - lo
+            for name, want, got in (("master", master, opt.master), ("m", m, opt.exp_avg), ("v", v, opt.exp_avg_sq)):
+                if not np.array_equal(got[o:o + n].cpu().numpy().view(np.uint32), want.view(np.uint32)):
+                    errors.append(f"bucket {bi}: {name}")
+            if not np.array_equal(u16(opt.param_buffer[lo:hi]), want_p):
+                errors.append(f"bucket {bi}: gathered params")
+            checked += n
+        out["elements_checked_per_rank"] = checked
+    ok = torch.tensor([0 if errors else 1], dtype=torch.int32, device=dev)
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    out["ok"] = bool(ok.item())
+    out["errors_rank"] = errors[:8]
+    out["seconds"] = round(time.perf_counter() - t0, 1)
+    return out
+
+
 def cpu_baseline(config: str, gs, seconds: float = 10.0) -> dict:
     """Oracle (CPU port) timed on a bounded sample: pack + AdamW over whole
     buckets of the workload, repeated until ``seconds`` elapse."""
@@ -231,34 +361,100 @@ def cpu_baseline(config: str, gs, seconds: float = 10.0) -> dict:
                       f"(d=1 step restated by oracle/hod_oracle.c, OpenMP {oracle.threads()} threads, {dt:.1f} s)"}
 
 
+_CPU_REF: dict = {}
+
+
+def cpu_reference_step(gs, d: int, clip, bucket_size: int, budget_s: float) -> dict:
+    """One optimizer step of the whole job restated on the host cores by the
+    oracle (oracle/hod_oracle.c, OpenMP): for every bucket, the pack of each of
+    the d ranks' gradients (dp-scale + bf16 cast), the rank-order reduce-scatter
+    sum, the clip norm and the AdamW update of every shard — the reference's
+    own CPU path for this step, since the reference has no optimizer.
+    Buckets stream through reused host buffers (the work and DRAM traffic per
+    bucket are those of the real step).  If the full step would exceed
+    ``budget_s`` the step is cut after the buckets that fit (a bounded sample,
+    labelled as such); params/s = parameters updated / seconds."""
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2312_03549_b200.buckets import build_bucket_layout
+
+    key = (gs.name, d, bucket_size)
+    if key not in _CPU_REF:
+        L = build_bucket_layout(gs.numels, bucket_size, dp=d)
+        rng = np.random.default_rng(0)
+        block = oracle.f32_to_bf16(rng.standard_normal(1 << 20, dtype=np.float32) * 1e-3)
+        big = max(b.numel for b in L.buckets)
+        grads = {t_i: (np.tile(block, -(-n // block.size))[:n] if n else np.zeros(0, np.uint16))
+                 for t_i, n in enumerate(gs.numels)}
+        _CPU_REF.clear()
+        _CPU_REF[key] = (L, grads, rng.standard_normal(big, dtype=np.float32) * 0.02,
+                         np.zeros(big, np.float32), np.zeros(big, np.float32))
+    L, grads, master, m, v = _CPU_REF[key]
+    t0 = time.perf_counter()
+    done = 0
+    nb = 0
+    for b in L.buckets:
+        srcs = [grads[s.index] for s in b.slots]
+        offs = [s.offset for s in b.slots]
+        packs = [oracle.pack(srcs, offs, b.numel, 1.0 / d) for _ in range(d)]
+        shards = [oracle.reduce_scatter(packs, r, d) if d > 1 else packs[0] for r in range(d)]
+        coef = None
+        if clip:
+            ss = sum(oracle.sumsq_bf16(x) for x in shards)
+            coef = oracle.clip_coef(np.float32(ss), clip)
+        n = b.numel // d
+        for r in range(d):
+            oracle.adamw(master[:n], m[:n], v[:n], shards[r], 1, coef=coef)
+        done += b.numel
+        nb += 1
+        if time.perf_counter() - t0 > budget_s and nb < len(L.buckets):
+            break
+    dt = time.perf_counter() - t0
+    full = nb == len(L.buckets)
+    return {"params": done, "seconds": dt, "buckets": nb, "of": len(L.buckets), "full": full}
+
+
 def run_reference(args) -> None:
-    """--impl reference: the CPU restatement of the same step on host cores."""
+    """--impl reference: the job's optimizer step on the host cores (rank 0
+    only; the other ranks exit 0 without work), same config / metric / unit."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    from oracle import oracle
+    from paper_2312_03549_b200.buckets import build_bucket_layout
     from paper_2312_03549_b200.gradsets import config_gradset
 
+    cfg = CONFIGS[args.config]
+    clip = cfg["clip"] if args.clip is None else (None if args.clip <= 0 else args.clip)
     gs = config_gradset(args.config)
-    times = []
-    base = None
+    d = args.gpus
+    cores = len(os.sched_getaffinity(0))
+    oracle.set_threads(cores)
+    vals, last = [], None
     for i in range(args.warmup + args.steps):
-        r = cpu_baseline(args.config, gs, seconds=max(1.0, args.ref_seconds / max(1, args.steps)))
+        r = cpu_reference_step(gs, d, clip, args.bucket_size, budget_s=args.ref_seconds)
         if i >= args.warmup:
-            times.append(r["value"])
-            base = r
-    value = statistics.median(times)
-    total = gs.total
+            vals.append(r["params"] / r["seconds"])
+            last = r
+    value = statistics.median(vals)
+    nbk = len(build_bucket_layout(gs.numels, args.bucket_size, dp=d).buckets)
+    sample = (f"{'full step' if last['full'] else 'bounded sample'}: {last['buckets']} of {last['of']} buckets "
+              f"x (pack of {d} ranks + reduce-scatter + {'clip + ' if clip else ''}AdamW) per timed step, "
+              f"oracle/hod_oracle.c OpenMP {oracle.threads()} threads"
+              + ("" if last["full"] else "; params/s extrapolates the sample to the step"))
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * total / value, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "warmup": args.warmup, "ms_per_step": 1e3 * gs.total / value, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16-grads/f32-adamw", "data": "synthetic",
         "impl": "reference",
-        "config": {"workload": CONFIGS[args.config]["desc"], "params": total, "bucket_size": 25_000_000,
-                   "world": world, "note": "reference has no optimizer (SPEC.md:14); CPU restatement timed"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": base["cores"], "kind": base["kind"],
-                         "sample": base["sample"]},
+        "config": _config_doc(args, clip, gs.total, nbk, d),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.threads(), "kind": "port",
+                         "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference has no optimizer implementation (SPEC.md:14): its CPU path for this step is "
+                "the oracle restatement (SURVEY §8c)",
     }
     print(json.dumps(line), flush=True)
 
@@ -301,16 +497,20 @@ def north_star_probe(args, world: int, rank: int, dev) -> dict:
 
     opt.pre_barrier = True   # the hook-driven default (register_hooks)
     o = measure(opt, gs, args.overlap_tokens, 3, world, dev)
+    opt.pre_barrier = False
+    parity = None if args.no_parity else parity_probe(opt, gs, rank, dev, torch.bfloat16, world)
     P, d = gs.total, world
     peak, _ = _peaks()
     hbm = 4 * P + 30 * P / d                  # pack + AdamW 28 B + norm read 2 B per owned element
     nvl = 4 * P * (d - 1) / d
-    t_roof = max(hbm / (peak * 1e9), nvl / (NVLINK_MEASURED * 1e9)) * 1e3
+    t_roof = max(hbm / (peak * 1e9), nvl / (NVLINK_PEAK * 1e9)) * 1e3
     out = {"workload": f"LLaMA-7B real tensor list, bf16 grads, grad-norm clip 1.0, DP={world} "
                        f"(BASELINE.json target; backend {opt.backend})",
            "params": gs.total, "ms_per_step": ms, "params_per_s": gs.total / (ms / 1e3), "steps": steps,
+           "parity": parity,
            "step_roofline": {"t_roof_ms": t_roof, "frac": t_roof / ms,
-                             "bound": "hbm" if hbm / (peak * 1e9) >= nvl / (NVLINK_MEASURED * 1e9) else "nvlink"},
+                             "nvlink_peak_gbps": NVLINK_PEAK,
+                             "bound": "hbm" if hbm / (peak * 1e9) >= nvl / (NVLINK_PEAK * 1e9) else "nvlink"},
            "overlap": {"tokens_per_gpu": args.overlap_tokens,
                        "exposed_frac_iteration": o["iteration"]["exposed_frac"],
                        "t_fwd_bwd_ms": o["iteration"]["t_fwd_bwd_ms"],
@@ -353,6 +553,7 @@ def scenario_probe(args, path: Path, world: int, rank: int, dev) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = _max_over_ranks(e0.elapsed_time(e1) / steps, world)
+    parity = None if args.no_parity else parity_probe(opt, gs, rank, dev, torch.bfloat16, world)
     gathered = [None] * world
     dist.all_gather_object(gathered, {sr.placement.stage: gs.total})
     totals = {}
@@ -360,7 +561,8 @@ def scenario_probe(args, path: Path, world: int, rank: int, dev) -> dict:
         totals.update(dct)
     out = {"scenario": path.name, "stage_layers": list(hp.partition_scenario(scenario).stage_layers),
            "stage_params": totals, "dp_ranks_rank0": list(sr.placement.dp_ranks), "backend": opt.backend,
-           "ms_per_step": ms, "params_per_s": sum(totals.values()) / (ms / 1e3), "steps": steps}
+           "ms_per_step": ms, "params_per_s": sum(totals.values()) / (ms / 1e3), "steps": steps,
+           "parity": parity}
     opt.close()
     del grads, opt
     torch.cuda.empty_cache()
@@ -399,8 +601,8 @@ def _sweep_row(doc: dict) -> dict:
             continue
         bus = v.get("busBW_GBps")
         row[k] = {"ms": v["ms"], "busBW_GBps": bus,
-                  "frac_nvlink": round(bus / NVLINK_MEASURED, 3) if bus else None,
-                  "frac_nvlink_nominal": round(bus / NVLINK_NOMINAL, 3) if bus else None}
+                  "frac_nvlink": round(bus / NVLINK_PEAK, 3) if bus else None,
+                  "frac_nvlink_measured_copy": round(bus / NVLINK_MEASURED, 3) if bus else None}
     return row
 
 
@@ -519,8 +721,8 @@ def run_ours(args) -> None:
         hbm = elems * hbm_elem / (ktime / 1e3) / 1e9 if ktime > 0 else None
         hbm_view = {"achieved": hbm, "peak": peak, "frac": hbm / peak if hbm else None,
                     "bytes_per_owned_element": hbm_elem}
-        nvl_view = {"achieved": nvl, "peak": NVLINK_MEASURED, "frac": nvl / NVLINK_MEASURED if nvl else None,
-                    "frac_nominal": nvl / NVLINK_NOMINAL if nvl else None,
+        nvl_view = {"achieved": nvl, "peak": NVLINK_PEAK, "frac": nvl / NVLINK_PEAK if nvl else None,
+                    "frac_measured_copy": nvl / NVLINK_MEASURED if nvl else None,
                     "bytes_per_owned_element": per_elem}
         if opt.backend == "nvls":
             # what the switch actually moves per GPU and direction (the larger of
@@ -529,14 +731,14 @@ def run_ours(args) -> None:
             nvl_view["physical_bytes_per_owned_element"] = phys
             nvl_view["physical_achieved"] = elems * phys / (ktime / 1e3) / 1e9 if ktime > 0 else None
         roof["traffic_emulated"] = _emulated_traffic_ratio(dom, d_, opt.backend)
-        if hbm_elem / peak >= per_elem / NVLINK_MEASURED:
+        if hbm_elem / peak >= per_elem / NVLINK_PEAK:
             roof.update({"bound": "hbm", "achieved": hbm, "frac": hbm_view["frac"],
                          "bytes_per_element": hbm_elem, "nvlink_view": nvl_view})
         else:
-            roof.update({"bound": "nvlink", "achieved": nvl, "peak": NVLINK_MEASURED, "frac": nvl_view["frac"],
-                         "peak_source": "NVLink 5 measured peer copy 770 GB/s/dir (B200_PROFILING.md); "
-                         "nominal 900 in frac_nominal",
-                         "frac_nominal": nvl_view["frac_nominal"], "hbm_view": hbm_view,
+            roof.update({"bound": "nvlink", "achieved": nvl, "peak": NVLINK_PEAK, "frac": nvl_view["frac"],
+                         "peak_source": "NVLink 5 nominal 900 GB/s per direction (north star, SURVEY §8d); "
+                         "frac_measured_copy against the 770 GB/s peer copy of B200_PROFILING.md",
+                         "frac_measured_copy": nvl_view["frac_measured_copy"], "hbm_view": hbm_view,
                          "nvlink_bytes_per_owned_element": per_elem, "bytes_per_element": per_elem})
             if "physical_achieved" in nvl_view:
                 roof["nvlink_physical"] = {k: nvl_view[k] for k in
@@ -554,15 +756,15 @@ def run_ours(args) -> None:
     else:
         hbm_bytes = (src_b + 2) * P + 28 * P / d + (2 * P / d if clip else 0)
     nvl_bytes = 4 * P * (d - 1) / d
-    # NVLink denominator: the measured 770 GB/s/dir peer copy (B200_PROFILING.md);
-    # the nominal-900 roofline (BASELINE.md's table) is reported beside it
-    t_roof = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / (NVLINK_MEASURED * 1e9)), world)
-    t_roof_nom = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / (NVLINK_NOMINAL * 1e9)), world)
+    # NVLink denominator: 900 GB/s per direction (north star, SURVEY §8d,
+    # BASELINE.md's table); the measured 770 GB/s peer copy is reported beside it
+    t_roof = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / (NVLINK_PEAK * 1e9)), world)
+    t_roof_meas = _max_over_ranks(max(hbm_bytes / (peak * 1e9), nvl_bytes / (NVLINK_MEASURED * 1e9)), world)
     step_roof = {"t_roof_ms": t_roof * 1e3, "frac": (t_roof * 1e3) / ms,
-                 "t_roof_nominal_ms": t_roof_nom * 1e3, "frac_nominal": (t_roof_nom * 1e3) / ms,
+                 "t_roof_measured_copy_ms": t_roof_meas * 1e3, "frac_measured_copy": (t_roof_meas * 1e3) / ms,
                  "hbm_bytes_per_gpu": hbm_bytes, "nvlink_bytes_per_gpu_per_dir": nvl_bytes,
-                 "nvlink_peak_gbps": NVLINK_MEASURED,
-                 "bound": "hbm" if hbm_bytes / (peak * 1e9) >= nvl_bytes / (NVLINK_MEASURED * 1e9) else "nvlink"}
+                 "nvlink_peak_gbps": NVLINK_PEAK,
+                 "bound": "hbm" if hbm_bytes / (peak * 1e9) >= nvl_bytes / (NVLINK_PEAK * 1e9) else "nvlink"}
 
     # ---- e2e through the public API with host buffers ---------------------
     e2e = None
@@ -616,6 +818,10 @@ def run_ours(args) -> None:
                            "exposed_frac_iteration = (iter with optimizer - iter without) / iter with"}
 
     opt_info = {"buckets": len(opt.layout.buckets), "dp": opt.dp, "backend": opt.backend}
+    # ---- self-check after every timed measurement (one more step vs the oracle)
+    parity = None
+    if not args.no_parity:
+        parity = _guarded("parity", lambda: parity_probe(opt, gs, rank, dev, gdtype, world), world)
     extras = None
     if args.extras == 1 or (args.extras == -1 and world >= 4 and not scen and args.config == "gpt1.3b"):
         # the driver's multi-GPU runs use the default config: measure the other
@@ -640,14 +846,8 @@ def run_ours(args) -> None:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16-grads/f32-adamw", "data": "synthetic",
-            "config": {"workload": (f"scenario {scen['scenario']}: GPT stages {scen['stage_layers']} "
-                                    "(reference self-adapting partition), PP x DP, world clip norm"
-                                    if scen else _desc(cfg, clip)),
-                       "config": "scenario" if scen else args.config, "params": params_per_step,
-                       "scenario": scen,
-                       "buckets": opt_info["buckets"], "bucket_size": args.bucket_size,
-                       "dp": opt_info["dp"], "clip": clip, "backend": opt_info["backend"],
-                       "l2": "inputs (~%.0f GB) >> 126 MB L2, no flush needed" % (hbm_bytes / 1e9)},
+            "config": _config_doc(args, clip, params_per_step, opt_info["buckets"], opt_info["dp"], scen),
+            "backend": opt_info["backend"], "parity": parity,
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "overlap": overlap, "extras": extras,
@@ -684,13 +884,17 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="skip the N > 1 iteration-exposure measurement")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-measurement self-check of sampled buckets against the oracle")
     ap.add_argument("--overlap-tokens", type=int, default=8192)
     ap.add_argument("--extras", type=int, default=-1, choices=[-1, 0, 1],
                     help="also measure BASELINE configs 3 (LLaMA-7B clip DP=N: step + iteration exposure), "
                          "4 (13B PP=2 x DP=N/2 scenario) and 5 (bucket sweep) at this N; "
                          "-1 = on for the default config at N >= 4")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--ref-seconds", type=float, default=30.0)
+    ap.add_argument("--ref-seconds", type=float, default=4.0,
+                    help="--impl reference: time budget of one timed CPU step (a longer step is cut to a "
+                         "bounded, labelled sample of its buckets)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)

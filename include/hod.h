@@ -171,6 +171,10 @@ int hod_adamw_f32(float* master, float* exp_avg, float* exp_avg_sq,
 int hod_nccl_unique_id(uint8_t out[128]);
 int hod_nccl_comm_init(const uint8_t id[128], int nranks, int rank, void** comm);
 int hod_comm_destroy(void* comm);
+/* HOD_OK, or HOD_ENCCL with the communicator's asynchronous error (a peer
+ * failure, a network error) in hod_last_error(): ncclCommGetAsyncError,
+ * polled by the host between steps without synchronising. */
+int hod_comm_async_error(void* comm);
 /* sum-reduce-scatter: recv (recvcount bf16) = sum over ranks of
  * send[rank*recvcount .. (rank+1)*recvcount).  In-place allowed when
  * recv == send + rank*recvcount. (prices: simulator.py:81-84) */

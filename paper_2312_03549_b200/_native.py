@@ -25,7 +25,7 @@ EXPORTED = (
     "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
     "hod_pack_bf16", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
     "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma", "hod_adamw", "hod_sumsq",
-    "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy",
+    "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy", "hod_comm_async_error",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
     "hod_p2p_step", "hod_p2p_barrier", "hod_p2p_norm", "hod_p2p_signal", "hod_p2p_wait", "hod_ce_copy",
 )
@@ -118,6 +118,7 @@ def load(build_if_missing: bool = True):
         "hod_nccl_unique_id": ([P], I),
         "hod_nccl_comm_init": ([P, I, I, ctypes.POINTER(ctypes.c_void_p)], I),
         "hod_comm_destroy": ([P], I),
+        "hod_comm_async_error": ([P], I),
         "hod_reduce_scatter_bf16": ([P, P, ctypes.c_size_t, P, P], I),
         "hod_all_gather_bf16": ([P, P, ctypes.c_size_t, P, P], I),
         "hod_all_reduce_f32": ([P, ctypes.c_size_t, P, P], I),

@@ -114,6 +114,12 @@ class NcclComm:
     def all_reduce_f32(self, ptr: int, n: int, stream) -> None:
         nat.call("hod_all_reduce_f32", ptr, n, self.handle, nat.stream_ptr(stream))
 
+    def check(self) -> None:
+        """Raise DeviceError if NCCL recorded an asynchronous error on this
+        communicator (ncclCommGetAsyncError; no synchronisation)."""
+        if self.handle:
+            nat.call("hod_comm_async_error", self.handle)
+
     def close(self) -> None:
         if self.handle:
             nat.call("hod_comm_destroy", self.handle)

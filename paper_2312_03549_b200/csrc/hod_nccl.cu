@@ -50,6 +50,15 @@ int hod_comm_destroy(void* comm) {
   return nccl_status(ncclCommDestroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
 }
 
+int hod_comm_async_error(void* comm) {
+  if (!comm) { hod::set_error("hod_comm_async_error: null"); return HOD_EINVAL; }
+  ncclResult_t async = ncclSuccess;
+  const int rc = nccl_status(ncclCommGetAsyncError(static_cast<ncclComm_t>(comm), &async),
+                             "ncclCommGetAsyncError");
+  if (rc) return rc;
+  return nccl_status(async, "NCCL communicator (asynchronous error)");
+}
+
 int hod_reduce_scatter_bf16(const void* send, void* recv, size_t recvcount, void* comm, void* stream) {
   if (!send || !recv || !comm) { hod::set_error("hod_reduce_scatter_bf16: null"); return HOD_EINVAL; }
   return nccl_status(ncclReduceScatter(send, recv, recvcount, ncclBfloat16, ncclSum,

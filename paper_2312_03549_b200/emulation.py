@@ -12,12 +12,15 @@ ranks' steps one after another without synchronising, and the GPU runs them
 concurrently, so every flag is raised by a real peer kernel (nothing is
 pre-arrived).
 
-Two things keep d ranks' spinning kernels from starving each other on one
+Three things keep d ranks' spinning kernels from starving each other on one
 GPU: a standing CTA cap (``grid_cap``) so that every rank's pack, span and
-barrier kernels fit on the 148 SMs at once, and enough hardware work queues
-(``CUDA_DEVICE_MAX_CONNECTIONS`` = 32, which must be set before CUDA
-initialises) so that a spinning kernel on one stream never blocks a kernel of
-another rank queued behind it.  NVLS multicast has no one-GPU stand-in
+barrier kernels fit on the 148 SMs at once; eager module loading
+(``CUDA_MODULE_LOADING=EAGER``) — with lazy loading, the first launch of a
+kernel that is not loaded yet waits behind a kernel already spinning on the
+device (measured, tools/emu_probe.py: a 3 s barrier timeout that disappears
+with EAGER); and enough hardware work queues (``CUDA_DEVICE_MAX_CONNECTIONS``
+= 32).  Both variables must be set before CUDA initialises, i.e. in the
+environment of a fresh process (``child_env()``).  NVLS multicast has no one-GPU stand-in
 (a multicast object binds one physical allocation per device), so only the
 p2p backend is emulated.  This is a test and profiling harness; production
 ranks get ``symm.SymmetricTensor``.
@@ -42,8 +45,17 @@ def grid_cap(d: int) -> int:
     return max(4, (2 * _SMS) // (3 * d))
 
 
+def child_env(env=None) -> dict:
+    """Environment for a process that runs emulated ranks."""
+    env = dict(os.environ if env is None else env)
+    env.update(CUDA_DEVICE_MAX_CONNECTIONS="32", CUDA_MODULE_LOADING="EAGER")
+    return env
+
+
 def connections_ok() -> bool:
-    return int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) >= 32
+    """True when this process was started with ``child_env()``."""
+    return (int(os.environ.get("CUDA_DEVICE_MAX_CONNECTIONS", "8")) >= 32
+            and os.environ.get("CUDA_MODULE_LOADING", "") == "EAGER")
 
 
 class EmulatedSymmetric:

@@ -580,7 +580,11 @@ class DistributedOptimizer:
 
     def poll_error(self) -> None:
         """Raise DeviceError if an earlier step's read-back error word is
-        nonzero.  Never blocks: a read-back still in flight is checked later."""
+        nonzero, or if a NCCL communicator holds an asynchronous error.
+        Never blocks: a read-back still in flight is checked later."""
+        for c in (self.comm, self.norm_comm):
+            if c is not None:
+                c.check()
         if self._err_pending and self._ev_err.query():
             self._err_pending = False
             raise_device_error(int(self._err_host[0]))
@@ -868,7 +872,10 @@ class DistributedOptimizer:
 
     def check_health(self) -> None:
         """Raise DeviceError if a cross-GPU barrier timed out or met a
-        mismatched span (synchronises)."""
+        mismatched span, or NCCL reported an asynchronous error (synchronises)."""
+        for c in (self.comm, self.norm_comm):
+            if c is not None:
+                c.check()
         raise_device_error(int(self._err.item()))
 
     def _norm_then_pack_adamw(self) -> None:

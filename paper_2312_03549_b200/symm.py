@@ -16,9 +16,26 @@ import torch.distributed as dist
 from .errors import DeviceError
 
 
-def _symm():
-    import torch.distributed._symmetric_memory as symm_mem
+# torch's symmetric memory is a private API: the calls used here exist with
+# these semantics from torch 2.6 on (empty / rendezvous / buffer_ptrs /
+# multicast_ptr); checked once, with a clear error instead of an AttributeError
+# deep inside a step
+_MIN_TORCH = (2, 6)
 
+
+def _symm():
+    ver = tuple(int(x) for x in torch.__version__.split("+")[0].split(".")[:2])
+    if ver < _MIN_TORCH:
+        raise DeviceError(f"torch {torch.__version__}: symmetric memory needs torch >= 2.6 "
+                          "(use backend='nccl')")
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+    except ImportError as e:
+        raise DeviceError(f"torch.distributed._symmetric_memory unavailable ({e}); use backend='nccl'") from e
+    for name in ("empty", "rendezvous"):
+        if not hasattr(symm_mem, name):
+            raise DeviceError(f"torch {torch.__version__}: _symmetric_memory.{name} missing; "
+                              "use backend='nccl'")
     return symm_mem
 
 
@@ -32,6 +49,8 @@ class SymmetricTensor:
             self.tensor.zero_()
         name = group.group_name if group is not None else dist.group.WORLD.group_name
         self.handle = symm_mem.rendezvous(self.tensor, name)
+        if not hasattr(self.handle, "buffer_ptrs"):
+            raise DeviceError(f"torch {torch.__version__}: symmetric memory handle has no buffer_ptrs")
         self.ptrs = [int(p) for p in self.handle.buffer_ptrs]
         self.mc = int(self.handle.multicast_ptr or 0)
         self.rank = int(self.handle.rank)

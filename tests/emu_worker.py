@@ -1,7 +1,7 @@
 """d DistributedOptimizer ranks of one DP row, concurrently on ONE GPU.
 
 Launched by tests/test_emulated_optimizer_gpu.py in a fresh process with
-CUDA_DEVICE_MAX_CONNECTIONS=32 (paper_2312_03549_b200/emulation.py).  Every
+CUDA_DEVICE_MAX_CONNECTIONS=32 CUDA_MODULE_LOADING=EAGER (emulation.child_env).  Every
 rank owns its optimizer, streams and buffers; peer pointers resolve to the
 other ranks' allocations, so arrival barriers, span tags, params-ready
 barriers and the peer-memory norm exchange all run for real, each flag raised
@@ -138,7 +138,7 @@ def main():
     ap.add_argument("--fault", default=None, choices=[None, "timeout", "span", "checkpoint"])
     a = ap.parse_args()
     if not connections_ok():
-        raise SystemExit("CUDA_DEVICE_MAX_CONNECTIONS must be >= 32 before CUDA initialises")
+        raise SystemExit("start with emulation.child_env(): CUDA_DEVICE_MAX_CONNECTIONS=32, CUDA_MODULE_LOADING=EAGER")
     dev = torch.device("cuda", 0)
     gs = config_gradset(a.config)
     gdt = torch.float32 if a.grad_dtype == "f32" else torch.bfloat16

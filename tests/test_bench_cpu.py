@@ -46,5 +46,26 @@ def test_sweep_row_fractions():
         "fused_p2p": {"ms": 2.5, "busBW_GBps": 616.0}, "adamw_local": {"ms": 0.1, "busBW_GBps": None},
         "error": 0}})
     assert row["bucket_MB"] == 1024.0
-    assert row["fused_p2p"] == {"ms": 2.5, "busBW_GBps": 616.0, "frac_nvlink": 0.8, "frac_nvlink_nominal": 0.684}
+    # headline denominator: 900 GB/s per direction (north star); measured copy beside it
+    assert row["fused_p2p"] == {"ms": 2.5, "busBW_GBps": 616.0, "frac_nvlink": 0.684,
+                                "frac_nvlink_measured_copy": 0.8}
     assert row["adamw_local"]["frac_nvlink"] is None and "error" not in row
+
+
+def test_reference_arm_config_equals_gpu_arm_config():
+    """Both arms build ``config`` with bench._config_doc from the same args, so
+    the driver's same-config check holds; the CPU sample is labelled."""
+    sys.path.insert(0, str(ROOT))
+    import argparse
+
+    import bench
+    from paper_2312_03549_b200.buckets import build_bucket_layout
+    from paper_2312_03549_b200.gradsets import config_gradset
+
+    r = _run({})
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][0])
+    gs = config_gradset("toy")
+    args = argparse.Namespace(config="toy", bucket_size=25_000_000)
+    nb = len(build_bucket_layout(gs.numels, 25_000_000, dp=1).buckets)
+    assert d["config"] == json.loads(json.dumps(bench._config_doc(args, None, gs.total, nb, 1)))
+    assert "full step" in d["cpu_baseline"]["sample"] or "bounded sample" in d["cpu_baseline"]["sample"]

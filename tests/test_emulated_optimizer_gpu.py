@@ -1,7 +1,7 @@
 """The full multi-rank protocol on ONE GPU (driver-visible d > 1 parity).
 
 Each case starts tests/emu_worker.py in a fresh process with
-CUDA_DEVICE_MAX_CONNECTIONS=32: d DistributedOptimizer ranks of one DP row
+CUDA_DEVICE_MAX_CONNECTIONS=32 and eager module loading: d DistributedOptimizer ranks of one DP row
 share the device (paper_2312_03549_b200/emulation.py) and run concurrently —
 arrival barriers with span tags, params-ready barriers, the 1-CTA pre-span
 barrier, the peer-memory norm exchange and the clip, every flag raised by a
@@ -13,7 +13,6 @@ leaving stale parameters.
 """
 
 import json
-import os
 import subprocess
 import sys
 from pathlib import Path
@@ -26,7 +25,9 @@ ROOT = Path(__file__).resolve().parent.parent
 
 
 def run_worker(*args, timeout=600):
-    env = dict(os.environ, CUDA_DEVICE_MAX_CONNECTIONS="32")
+    from paper_2312_03549_b200.emulation import child_env
+
+    env = child_env()
     p = subprocess.run([sys.executable, str(ROOT / "tests" / "emu_worker.py"), *map(str, args)],
                        capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
     assert p.returncode == 0, f"worker failed ({p.returncode}):\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
