@@ -65,6 +65,13 @@ typedef struct hod_pack_entry {
   int64_t dst_offset;
 } hod_pack_entry;
 
+/* AdamW arithmetic: EXACT = IEEE operations in the oracle's order (bit-exact
+ * against oracle/hod_oracle.c; ~90 instructions per element); FAST = the same
+ * algebra with FMAs and MUFU sqrt/reciprocal (~25 instructions per element),
+ * within the north star's 1e-6 (1 step) / 1e-5 (100 steps) tolerance. */
+#define HOD_ADAMW_EXACT 0
+#define HOD_ADAMW_FAST 1
+
 /* AdamW hyper-parameters for one step.  The library folds them into fp32
  * constants exactly as documented in DESIGN.md §K2 (decoupled weight decay,
  * torch.optim.AdamW algebra). */
@@ -75,6 +82,8 @@ typedef struct hod_adamw_params {
   double eps;
   double weight_decay;
   int64_t step; /* 1-based step count used for bias correction */
+  int32_t mode; /* HOD_ADAMW_EXACT (default) or HOD_ADAMW_FAST */
+  int32_t reserved;
 } hod_adamw_params;
 
 /* ---- version / errors ---------------------------------------------------- */
@@ -82,7 +91,8 @@ int hod_abi_version(void);
 const char* hod_last_error(void);
 /* number of kernels this library has launched in the process (all streams) */
 long long hod_launch_count(void);
-/* Cap every subsequent launch of the calling thread at `max_ctas` CTAs
+/* Cap every subsequent launch of the process (all threads: autograd issues
+ * hook-driven launches from its own device thread) at `max_ctas` CTAs
  * (0 = no cap).  The overlapped optimizer sets it while backward GEMMs run so
  * its kernels occupy a bounded slice of the 148 SMs (pair with cuBLAS's SM
  * carve-out); partial-sum kernels use min(cap, HOD_SUMSQ_PARTIALS) CTAs and

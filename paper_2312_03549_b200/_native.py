@@ -67,9 +67,13 @@ class P2PSpan(ctypes.Structure):
     ]
 
 
+HOD_ADAMW_EXACT, HOD_ADAMW_FAST = 0, 1
+
+
 class AdamWParams(ctypes.Structure):
     _fields_ = [("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
-                ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("step", ctypes.c_int64)]
+                ("eps", ctypes.c_double), ("weight_decay", ctypes.c_double), ("step", ctypes.c_int64),
+                ("mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 ABI_VERSION = 2          # HOD_ABI_VERSION of include/hod.h
@@ -148,7 +152,7 @@ def call(name: str, *args) -> None:
 
 
 def set_grid_base(max_ctas: int) -> None:
-    """Standing CTA cap of every launch of this thread (0 = none).  The
+    """Standing CTA cap of every launch of this process (0 = none).  The
     optimizer's temporary ``sm_budget`` caps are taken relative to it and
     restore it afterwards (emulation.EmulatedRow keeps d ranks' kernels
     co-resident on one GPU with it)."""

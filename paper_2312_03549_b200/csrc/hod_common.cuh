@@ -110,9 +110,15 @@ __device__ __forceinline__ uint2 pack4(const float* f) {
                     static_cast<uint32_t>(f32_to_bf16(f[2])) | (static_cast<uint32_t>(f32_to_bf16(f[3])) << 16));
 }
 
+// fast mode: hardware RNE (cvt.rn.bf16x2; NaN payloads are not preserved)
+__device__ __forceinline__ uint2 pack4_hw(const float* f) {
+  return make_uint2(cvt_bf16x2_rn(f[0], f[1]), cvt_bf16x2_rn(f[2], f[3]));
+}
+
+template <bool kHw = false>
 __device__ __forceinline__ void st_bf16_quads(uint16_t* p, int64_t e0, const float (&x)[8]) {
-  *reinterpret_cast<uint2*>(p + e0) = pack4(x);
-  *reinterpret_cast<uint2*>(p + e0 + 128) = pack4(x + 4);
+  *reinterpret_cast<uint2*>(p + e0) = kHw ? pack4_hw(x) : pack4(x);
+  *reinterpret_cast<uint2*>(p + e0 + 128) = kHw ? pack4_hw(x + 4) : pack4(x + 4);
 }
 
 // Fp32 AdamW constants folded on the host in double precision, then rounded
@@ -124,18 +130,42 @@ struct AdamWConsts {
   float step_size;  // lr / (1 - beta1^t)
   float bc2_sqrt;   // sqrt(1 - beta2^t)
   float eps;
+  float inv_bc2_sqrt;   // 1 / sqrt(1 - beta2^t)        (fast mode)
+  float neg_step_size;  // -lr / (1 - beta1^t)          (fast mode)
+  int fast;             // HOD_ADAMW_FAST: launchers pick the kFast kernels
 };
 
 AdamWConsts fold_adamw(const hod_adamw_params& hp);
 
-// One element of the update; identical op order to oracle/hod_oracle.c.
+// One element of the update.
+//  exact (kFast = false): identical IEEE operations in the identical order as
+//    oracle/hod_oracle.c (explicit _rn intrinsics, no FMA contraction, IEEE
+//    sqrt and divisions): bit-exact against the oracle.
+//  fast (kFast = true, HOD_ADAMW_FAST): the same algebra in ~10 FP operations —
+//    FMAs, MUFU square root and reciprocal (sqrt.approx / rcp.approx, <= 2 ulp
+//    each), the bias correction folded into constants.  The update term
+//    lr*m/(sqrt(v)+eps) carries a few ulp of relative error, i.e. ~1e-9 of
+//    |theta| at lr = 1e-4; m and v differ from the exact mode by <= 1 ulp per
+//    step (FMA rounding): inside the north star's 1e-6 (1 step) / 1e-5
+//    (100 steps) tolerance (tests/test_kernels_gpu.py measures it).
+template <bool kFast = false>
 __device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g,
                                            const AdamWConsts& c) {
-  p = __fmul_rn(p, c.decay);
-  m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, g));
-  v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.omb2, __fmul_rn(g, g)));
-  const float den = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.bc2_sqrt), c.eps);
-  p = __fsub_rn(p, __fmul_rn(c.step_size, __fdiv_rn(m, den)));
+  if constexpr (kFast) {
+    m = fmaf(c.b1, m, c.omb1 * g);
+    v = fmaf(c.b2, v, (c.omb2 * g) * g);
+    float s, r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(s) : "f"(v));
+    const float den = fmaf(s, c.inv_bc2_sqrt, c.eps);
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(den));
+    p = fmaf(p, c.decay, c.neg_step_size * (m * r));
+  } else {
+    p = __fmul_rn(p, c.decay);
+    m = __fadd_rn(__fmul_rn(c.b1, m), __fmul_rn(c.omb1, g));
+    v = __fadd_rn(__fmul_rn(c.b2, v), __fmul_rn(c.omb2, __fmul_rn(g, g)));
+    const float den = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), c.bc2_sqrt), c.eps);
+    p = __fsub_rn(p, __fmul_rn(c.step_size, __fdiv_rn(m, den)));
+  }
 }
 
 // CTA cap set by hod_set_grid_limit (0 = none): lets the optimizer's kernels

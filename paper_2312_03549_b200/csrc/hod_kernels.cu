@@ -22,8 +22,10 @@ static std::atomic<long long> g_launches{0};
 
 void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
-static thread_local int g_grid_limit = 0;
-int grid_limit() { return g_grid_limit; }
+// process-wide: autograd runs post-accumulate-grad hooks (hence bucket
+// launches) on its own device thread, which must see the same cap
+static std::atomic<int> g_grid_limit{0};
+int grid_limit() { return g_grid_limit.load(std::memory_order_relaxed); }
 
 bool pdl_enabled() {
   static const bool v = [] {
@@ -67,6 +69,9 @@ AdamWConsts fold_adamw(const hod_adamw_params& hp) {
   c.step_size = static_cast<float>(hp.lr / bc1);
   c.bc2_sqrt = static_cast<float>(sqrt(bc2));
   c.eps = static_cast<float>(hp.eps);
+  c.inv_bc2_sqrt = static_cast<float>(1.0 / sqrt(bc2));
+  c.neg_step_size = static_cast<float>(-hp.lr / bc1);
+  c.fast = hp.mode == HOD_ADAMW_FAST;
   return c;
 }
 
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
 // result is bit-identical to pack followed by AdamW while the 2+2 B/element
 // bucket round trip disappears (28 B/element instead of 32).
 // ---------------------------------------------------------------------------
-template <typename SrcT, bool kClip>
+template <typename SrcT, bool kClip, bool kFast>
 __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
     const __grid_constant__ PackTable t, int64_t numel, float scale, float* __restrict__ p,
     float* __restrict__ m, float* __restrict__ v, uint16_t* __restrict__ out, const AdamWConsts c,
@@ -184,12 +189,12 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
       for (int k = 0; k < 8; ++k) {
         g[k] = bf16_to_f32(f32_to_bf16(__fmul_rn(g[k], scale)));
         if (kClip) g[k] = __fmul_rn(g[k], coef);
-        adamw_elem(pf[k], mf[k], vf[k], g[k], c);
+        adamw_elem<kFast>(pf[k], mf[k], vf[k], g[k], c);
       }
       st_f32_quads(p, e0, pf);
       st_f32_quads(m, e0, mf);
       st_f32_quads(v, e0, vf);
-      st_bf16_quads(out, e0, pf);
+      st_bf16_quads<kFast>(out, e0, pf);
     } else {
       int ei = e;
       for (int64_t i = a + lane; i < b; i += 32) {
@@ -199,7 +204,7 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
           gi = bf16_to_f32(f32_to_bf16(__fmul_rn(load_src<SrcT>(t.src[ei], i - t.off[ei]), scale)));
         if (kClip) gi = __fmul_rn(gi, coef);
         float pi = p[i], mi = m[i], vi = v[i];
-        adamw_elem(pi, mi, vi, gi, c);
+        adamw_elem<kFast>(pi, mi, vi, gi, c);
         p[i] = pi; m[i] = mi; v[i] = vi;
         out[i] = f32_to_bf16(pi);
       }
@@ -212,7 +217,7 @@ __global__ void __launch_bounds__(kThreads) pack_adamw_kernel(
 // bf16 grad, two 16-byte loads each of master/m/v; stores mirror them plus a
 // 16-byte bf16 param store.  28 B/element algorithmic traffic.
 // ---------------------------------------------------------------------------
-template <typename GradT, bool kClip>
+template <typename GradT, bool kClip, bool kFast>
 __global__ void __launch_bounds__(kThreads) adamw_vec_kernel(
     float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
     const GradT* __restrict__ g, uint16_t* __restrict__ out, int64_t n_chunks,
@@ -231,16 +236,16 @@ __global__ void __launch_bounds__(kThreads) adamw_vec_kernel(
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const float gk = kClip ? __fmul_rn(gf[k], coef) : gf[k];
-      adamw_elem(pf[k], mf[k], vf[k], gk, c);
+      adamw_elem<kFast>(pf[k], mf[k], vf[k], gk, c);
     }
     st_f32_quads(p, e0, pf);
     st_f32_quads(m, e0, mf);
     st_f32_quads(v, e0, vf);
-    st_bf16_quads(out, e0, pf);
+    st_bf16_quads<kFast>(out, e0, pf);
   }
 }
 
-template <typename GradT, bool kClip>
+template <typename GradT, bool kClip, bool kFast>
 __global__ void __launch_bounds__(kThreads) adamw_scalar_kernel(
     float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
     const GradT* __restrict__ g, uint16_t* __restrict__ out, int64_t begin, int64_t n,
@@ -252,7 +257,7 @@ __global__ void __launch_bounds__(kThreads) adamw_scalar_kernel(
     if constexpr (sizeof(GradT) == 2) gi = bf16_to_f32(g[i]); else gi = g[i];
     if (kClip) gi = __fmul_rn(gi, coef);
     float pi = p[i], mi = m[i], vi = v[i];
-    adamw_elem(pi, mi, vi, gi, c);
+    adamw_elem<kFast>(pi, mi, vi, gi, c);
     p[i] = pi; m[i] = mi; v[i] = vi;
     out[i] = f32_to_bf16(pi);
   }
@@ -278,20 +283,22 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
       // 2 CTAs/SM measured best (6.3 TB/s vs 5.9 TB/s at 4-8/SM; tools/sweep_grid.sh)
       const int grid = grid_for(n_vec * 32, kThreads, 2);
       count_launch(1);
-      if (clip_coef)
-        adamw_vec_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef);
-      else
-        adamw_vec_kernel<GradT, false><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, nullptr);
+#define HOD_AV(CLIP, FAST) \
+      adamw_vec_kernel<GradT, CLIP, FAST><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef)
+      if (clip_coef) { if (c.fast) HOD_AV(true, true); else HOD_AV(true, false); }
+      else { if (c.fast) HOD_AV(false, true); else HOD_AV(false, false); }
+#undef HOD_AV
     }
     done = n_vec * kChunk;
   }
   if (done < n) {
     const int grid = grid_for(n - done, kThreads);
     count_launch(1);
-    if (clip_coef)
-      adamw_scalar_kernel<GradT, true><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, clip_coef);
-    else
-      adamw_scalar_kernel<GradT, false><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, nullptr);
+#define HOD_AS(CLIP, FAST) \
+    adamw_scalar_kernel<GradT, CLIP, FAST><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, clip_coef)
+    if (clip_coef) { if (c.fast) HOD_AS(true, true); else HOD_AS(true, false); }
+    else { if (c.fast) HOD_AS(false, true); else HOD_AS(false, false); }
+#undef HOD_AS
   }
   return cuda_status(cudaGetLastError(), "hod_adamw launch");
 }
@@ -509,7 +516,7 @@ long long hod_launch_count(void) { return g_launches.load(std::memory_order_rela
 
 int hod_set_grid_limit(int max_ctas) {
   if (max_ctas < 0) { set_error("hod_set_grid_limit: negative limit"); return HOD_EINVAL; }
-  g_grid_limit = max_ctas;
+  g_grid_limit.store(max_ctas, std::memory_order_relaxed);
   return HOD_OK;
 }
 
@@ -559,13 +566,16 @@ int hod_pack_adamw(const hod_pack_entry* entries, int n_entries, int64_t bucket_
     float* ep = exp_avg + lo;
     float* vp = exp_avg_sq + lo;
     uint16_t* pp = param + lo;
-#define HOD_PA_LAUNCH(T, CLIP) \
-    launch_pdl(pack_adamw_kernel<T, CLIP>, grid, kThreads, s, t, span, scale, mp, ep, vp, pp, c, clip_coef)
+#define HOD_PA_LAUNCH(T, CLIP, FAST) \
+    launch_pdl(pack_adamw_kernel<T, CLIP, FAST>, grid, kThreads, s, t, span, scale, mp, ep, vp, pp, c, clip_coef)
+#define HOD_PA_FAST(T, CLIP) \
+    do { if (c.fast) HOD_PA_LAUNCH(T, CLIP, true); else HOD_PA_LAUNCH(T, CLIP, false); } while (0)
     if (src_dtype == HOD_DTYPE_BF16) {
-      if (clip_coef) HOD_PA_LAUNCH(uint16_t, true); else HOD_PA_LAUNCH(uint16_t, false);
+      if (clip_coef) HOD_PA_FAST(uint16_t, true); else HOD_PA_FAST(uint16_t, false);
     } else {
-      if (clip_coef) HOD_PA_LAUNCH(float, true); else HOD_PA_LAUNCH(float, false);
+      if (clip_coef) HOD_PA_FAST(float, true); else HOD_PA_FAST(float, false);
     }
+#undef HOD_PA_FAST
 #undef HOD_PA_LAUNCH
     return cuda_status(cudaGetLastError(), "hod_pack_adamw launch");
   });

@@ -278,7 +278,7 @@ __device__ __forceinline__ void gather_store4(const SpanArgs& a, int64_t e, cons
   }
 }
 
-template <int D, int kSrc, int kMode, int W>
+template <int D, int kSrc, int kMode, int W, bool kFast>
 __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSrc, W>& it,
                                             const AdamWConsts& c, float coef, float& ss) {
   using ItemT = Item<D, kSrc, W>;
@@ -351,19 +351,19 @@ __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSr
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       const float gk = (kMode == 2 && a.coef) ? __fmul_rn(g[k], coef) : g[k];
-      adamw_elem(pf[k], mf[k], vf[k], gk, c);
+      adamw_elem<kFast>(pf[k], mf[k], vf[k], gk, c);
     }
     *reinterpret_cast<float4*>(a.master + it.s[h]) = make_float4(pf[0], pf[1], pf[2], pf[3]);
     *reinterpret_cast<float4*>(a.m + it.s[h]) = make_float4(mf[0], mf[1], mf[2], mf[3]);
     *reinterpret_cast<float4*>(a.v + it.s[h]) = make_float4(vf[0], vf[1], vf[2], vf[3]);
-    gather_store4<D, kSrc>(a, it.e[h], pack4(pf));
+    gather_store4<D, kSrc>(a, it.e[h], kFast ? pack4_hw(pf) : pack4(pf));
   }
 }
 
 // kMode: 0 = fused RS+AdamW+AG, 1 = RS only (+in-place reduced shard, partials),
 // 2 = AdamW+AG from the in-place reduced shard.  U: items per thread in flight
 // (memory-level parallelism for the NVLink loads).
-template <int D, int kSrc, int kMode, int U, int W>
+template <int D, int kSrc, int kMode, int U, int W, bool kFast>
 __global__ void __launch_bounds__(kThreads, HOD_P2P_MINB) p2p_step_kernel(const __grid_constant__ SpanArgs a,
                                                              const BarrierArgs b, const AdamWConsts c,
                                                              int rank) {
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, HOD_P2P_MINB) p2p_step_kernel(const 
       load_item<D, kSrc, kMode, W>(a, it[u], rank);
     }
 #pragma unroll
-    for (int u = 0; u < U; ++u) finish_item<D, kSrc, kMode, W>(a, it[u], c, coef, ss);
+    for (int u = 0; u < U; ++u) finish_item<D, kSrc, kMode, W, kFast>(a, it[u], c, coef, ss);
   }
   if (kMode == 1 && a.partials) {
     const float s = block_sum_f(ss);
@@ -480,6 +480,14 @@ static int wide_setting() {
   return w;
 }
 
+template <int D, int kSrc, int kMode, int U, int W>
+static void launch_u_w(const SpanArgs& a, const BarrierArgs& b, const AdamWConsts& c, int rank, int grid,
+                       cudaStream_t s) {
+  // the RS half has no update: only the exact instantiation exists
+  if (kMode != 1 && c.fast) p2p_step_kernel<D, kSrc, kMode, U, W, kMode != 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+  else p2p_step_kernel<D, kSrc, kMode, U, W, false><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+}
+
 template <int D, int kSrc, int kMode>
 static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWConsts& c, int rank,
                         int grid, cudaStream_t s) {
@@ -490,11 +498,11 @@ static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWCons
   const bool two = u >= 2 || (u == 0 && D == 2);
   const int w = wide_setting();
   if (kSrc == kSrcPeer && kMode != 2 && (w > 0 || (w < 0 && D == 2))) {
-    if (two) p2p_step_kernel<D, kSrc, kMode, 2, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
-    else p2p_step_kernel<D, kSrc, kMode, 1, 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+    if (two) launch_u_w<D, kSrc, kMode, 2, 1>(a, b, c, rank, grid, s);
+    else launch_u_w<D, kSrc, kMode, 1, 1>(a, b, c, rank, grid, s);
   } else {
-    if (two) p2p_step_kernel<D, kSrc, kMode, 2, 0><<<grid, kThreads, 0, s>>>(a, b, c, rank);
-    else p2p_step_kernel<D, kSrc, kMode, 1, 0><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+    if (two) launch_u_w<D, kSrc, kMode, 2, 0>(a, b, c, rank, grid, s);
+    else launch_u_w<D, kSrc, kMode, 1, 0>(a, b, c, rank, grid, s);
   }
 }
 

@@ -136,6 +136,10 @@ class DistributedOptimizer:
     norm_ranks : ranks over which the clip norm is summed (default: the DP
         row; the whole world for PP x DP so every stage sees one norm).
     grad_scale : multiplier fused into the pack (default 1/d: gradient mean).
+    adamw : ``"exact"`` (default: IEEE operations in the oracle's order,
+        bit-exact against it) or ``"fast"`` (FMAs + MUFU sqrt/reciprocal,
+        ~25 instead of ~90 instructions per element; within the north star's
+        1e-6 / 1e-5 tolerance — include/hod.h HOD_ADAMW_FAST).
     symmetric, norm_symmetric : factories ``(numel, dtype, device, zero) ->``
         symmetric buffer (``.tensor``, ``.peer(q)``, ``.multicast()``, ``.mc``,
         ``.rank``, ``.world``) for the DP row / the clip-norm ranks; default:
@@ -152,7 +156,8 @@ class DistributedOptimizer:
                  keep_reduced: bool = False, barrier_timeout_s: float = 20.0,
                  sm_budget: int | None = None, span_numel: int = 256 * 2**20,
                  param_barriers: bool = True, pre_barrier: bool | None = None,
-                 first_span_numel: int | None = None, symmetric=None, norm_symmetric=None):
+                 first_span_numel: int | None = None, symmetric=None, norm_symmetric=None,
+                 adamw: str = "exact"):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         init_params = list(init_params)
@@ -162,6 +167,9 @@ class DistributedOptimizer:
                        else torch.device(device))
         self.lr, self.betas, self.eps, self.weight_decay = lr, tuple(betas), eps, weight_decay
         self.clip = clip
+        if adamw not in ("exact", "fast"):
+            raise InfeasibleConfigError(f"adamw must be 'exact' or 'fast', got {adamw!r}")
+        self.adamw_mode = adamw
         self.group = dp_group or DPGroup.single(0)
         self.dp = self.group.size
         self.shard_index = self.group.index
@@ -564,6 +572,43 @@ class DistributedOptimizer:
             handles.append(p.register_post_accumulate_grad_hook(hook))
         return handles
 
+    def attach(self, model) -> list:
+        """Bind ``model`` (an nn.Module whose ``parameters()`` are, in order,
+        the optimizer's registration order) to the flat buffers:
+
+        * every parameter's storage becomes its view of the bf16 param buffer
+          (the forward reads what the all-gather wrote);
+        * post-accumulate-grad hooks deliver gradients (``register_hooks``):
+          buckets launch during backward, in backward order;
+        * a forward pre-hook on every submodule that owns parameters waits
+          for their buckets (``wait_params``): after ``finish_step(wait=False)``
+          the all-gather of the last spans overlaps the next forward.
+
+        This is the integration point of the imported overlapped optimizer
+        (Megatron-LLaMA) that the reference prices as
+        non-overlapped.  Returns the hook handles."""
+        params = list(model.parameters())
+        if len(params) != len(self.params):
+            raise InfeasibleConfigError(f"model has {len(params)} parameters, optimizer {len(self.params)}")
+        index = {}
+        for i, (p, view) in enumerate(zip(params, self.params)):
+            if tuple(p.shape) != tuple(view.shape):
+                raise InfeasibleConfigError(f"parameter {i}: shape {tuple(p.shape)} vs {tuple(view.shape)}")
+            p.data = view
+            index[id(p)] = i
+        handles = self.register_hooks(params)
+        for mod in model.modules():
+            own = [index[id(p)] for p in mod.parameters(recurse=False) if id(p) in index]
+            if not own:
+                continue
+            buckets = sorted({self.layout.slot(i).bucket for i in own})
+
+            def pre(_mod, _inp, buckets=buckets):
+                for b in buckets:
+                    self.wait_params(b)
+            handles.append(mod.register_forward_pre_hook(pre))
+        return handles
+
     def no_sync(self):
         """Context manager: hooks registered by ``register_hooks`` do not
         deliver gradients inside it (gradient-accumulation micro-batches)."""
@@ -597,7 +642,8 @@ class DistributedOptimizer:
     # ------------------------------------------------------------ internals
     def _hp(self) -> nat.AdamWParams:
         return nat.AdamWParams(self.lr, self.betas[0], self.betas[1], self.eps, self.weight_decay,
-                               self.step_count)
+                               self.step_count,
+                               nat.HOD_ADAMW_FAST if self.adamw_mode == "fast" else nat.HOD_ADAMW_EXACT)
 
     def _grad_shard(self, b) -> tuple[int, int]:
         """(ptr, numel) of this rank's reduced-gradient shard of bucket b."""

@@ -53,7 +53,7 @@ def build(a, row, dev, gs, span_numel=None):
             dp_group=DPGroup(tuple(range(a.d)), r), backend="p2p", keep_reduced=bool(a.keep_reduced),
             barrier_timeout_s=a.timeout, span_numel=(span_numel[r] if span_numel else a.span),
             first_span_numel=(span_numel[r] if span_numel else a.first_span),
-            symmetric=row.factory(r), pre_barrier=(a.flow == "hooks")))
+            symmetric=row.factory(r), pre_barrier=(a.flow == "hooks"), adamw=a.adamw))
     return opts
 
 
@@ -116,6 +116,17 @@ def check(a, opts, gs, step, grads, state, reps):
                 assert np.array_equal(gbuf[lo:lo + n], reduced[bi][r]), f"step {step} rank {r} bucket {bi}: RS"
             master, m, v = (x[offs[bi]:offs[bi] + n] for x in state[r])
             want = oracle.adamw(master, m, v, reduced[bi][r], step, coef=coef)
+            if getattr(a, "adamw", "exact") == "fast":
+                # north-star tolerance (SURVEY §8d norm-relative rule); params
+                # are the RNE of the device's own master
+                rtol = 1e-6 if step == 1 else 1e-5
+                for name, dv, ov in zip(("master", "m", "v"), dev_state, (master, m, v)):
+                    got = dv[offs[bi]:offs[bi] + n].astype(np.float64)
+                    err = np.abs(got - ov).max() / max(np.abs(ov).max(), 1e-30)
+                    assert err <= rtol, f"step {step} rank {r} bucket {bi}: {name} rel err {err}"
+                own = torch.from_numpy(dev_state[0][offs[bi]:offs[bi] + n]).to(torch.bfloat16)
+                assert np.array_equal(params[0][lo:lo + n], u16(own)), f"step {step} rank {r} bucket {bi}: params"
+                continue
             assert np.array_equal(params[0][lo:lo + n], want), f"step {step} rank {r} bucket {bi}: params"
             for name, dv, ov in zip(("master", "m", "v"), dev_state, (master, m, v)):
                 assert np.array_equal(dv[offs[bi]:offs[bi] + n].view(np.uint32), ov.view(np.uint32)), \
@@ -135,6 +146,7 @@ def main():
     ap.add_argument("--flow", default="step", choices=["step", "hooks"])
     ap.add_argument("--keep-reduced", type=int, default=1)
     ap.add_argument("--timeout", type=float, default=10.0)
+    ap.add_argument("--adamw", default="exact", choices=["exact", "fast"])
     ap.add_argument("--fault", default=None, choices=[None, "timeout", "span", "checkpoint"])
     a = ap.parse_args()
     if not connections_ok():

@@ -87,9 +87,9 @@ def test_struct_layouts_match_c(tmp_path):
     gxx = shutil.which("g++") or "/usr/bin/g++"
     fields = {"hod_p2p_span": (nat.P2PSpan, ["local_grad", "master", "partials", "err", "bucket_start",
                                              "shard_numel", "n_buckets", "keep_reduced", "slot",
-                                             "epoch", "timeout_ns"]),
+                                             "epoch", "tag", "timeout_ns"]),
               "hod_pack_entry": (nat.PackEntry, ["src", "numel", "dst_offset"]),
-              "hod_adamw_params": (nat.AdamWParams, ["lr", "weight_decay", "step"])}
+              "hod_adamw_params": (nat.AdamWParams, ["lr", "weight_decay", "step", "mode"])}
     lines = ['#include <cstdio>', '#include <cstddef>', '#include "hod.h"', "int main() {"]
     for cname, (_, names) in fields.items():
         lines.append(f'  printf("%zu\\n", sizeof({cname}));')

@@ -47,6 +47,14 @@ def test_emulated_fp32_grads_without_keep_reduced():
     assert out["ok"]
 
 
+@pytest.mark.parametrize("d,clip", [(2, 0.0), (4, 0.02)])
+def test_emulated_ranks_fast_adamw_within_tolerance(d, clip):
+    """adamw='fast' through the fused span kernels: reduce-scatter still
+    bit-exact, master / m / v within the north star's tolerance."""
+    out = run_worker("--d", d, "--clip", clip, "--adamw", "fast", "--steps", 3)
+    assert out["ok"]
+
+
 def test_barrier_timeout_raises_device_error():
     out = run_worker("--d", 2, "--fault", "timeout", "--timeout", 0.5)
     assert "10003" in out["raised"] and "next_step_raised" in out

@@ -101,9 +101,9 @@ def test_pack_adamw_fused_equals_pack_then_adamw(oracle, native, src_dtype, clip
         np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), cp.view(np.uint32))
 
 
-def _adamw_gpu(master, m, v, grad, n, step, coef=None, out_offset=0):
+def _adamw_gpu(master, m, v, grad, n, step, coef=None, out_offset=0, mode=0):
     out = torch.empty(n + out_offset, dtype=torch.bfloat16, device=DEV)
-    hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, step)
+    hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, step, mode)
     fn = "hod_adamw_f32" if grad.dtype == torch.float32 else "hod_adamw_bf16"
     coef_ptr = None if coef is None else coef.data_ptr()
     nat.call(fn, master.data_ptr(), m.data_ptr(), v.data_ptr(), grad.data_ptr(),
@@ -132,6 +132,42 @@ def test_adamw_bit_exact_100_steps(oracle, native, n, offset, grad_dtype):
             np.testing.assert_array_equal(m.cpu().numpy().view(np.uint32), cv.view(np.uint32))
             np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), cp.view(np.uint32))
             np.testing.assert_array_equal(u16(p), want_p)
+
+
+def _norm_rel(gpu, cpu):
+    """SURVEY §8d pass rule: ||gpu - cpu||_inf / ||cpu||_inf."""
+    gpu, cpu = np.asarray(gpu, np.float64), np.asarray(cpu, np.float64)
+    return float(np.abs(gpu - cpu).max() / max(np.abs(cpu).max(), 1e-30))
+
+
+@pytest.mark.parametrize("n,offset", [(1_000_003, 0), (65_536, 1)])
+@pytest.mark.parametrize("clip", [None, 0.37])
+def test_adamw_fast_mode_within_north_star_tolerance(oracle, native, n, offset, clip):
+    """HOD_ADAMW_FAST (FMAs, MUFU sqrt / reciprocal) against the exact oracle:
+    master / m / v within 1e-6 norm-relative after 1 step and 1e-5 after
+    100 (the north star's tolerance, SURVEY §8d rule); the bf16 params are
+    the RNE of the device's own master."""
+    gen = torch.Generator(device=DEV).manual_seed(n + 5)
+    base = torch.randn(n + offset, generator=gen, device=DEV).mul_(0.02)
+    master = base[offset:].clone() if offset == 0 else base[offset:]
+    m = torch.zeros(n + offset, device=DEV)[offset:]
+    v = torch.zeros(n + offset, device=DEV)[offset:]
+    coef = None if clip is None else torch.tensor([clip], device=DEV)
+    cm, cv, cp = (master.cpu().numpy().copy(), np.zeros(n, np.float32), np.zeros(n, np.float32))
+    worst = {}
+    for step in range(1, 101):
+        g = torch.randn(n + offset, generator=gen, device=DEV).mul_(1e-3).to(torch.bfloat16)[offset:]
+        p = _adamw_gpu(master, m, v, g, n, step, coef=coef, mode=nat.HOD_ADAMW_FAST)
+        oracle.adamw(cm, cv, cp, u16(g), step, coef=None if clip is None else np.float32(clip))
+        if step in (1, 100):
+            torch.cuda.synchronize()
+            rtol = 1e-6 if step == 1 else 1e-5
+            for name, dev_t, ref in (("master", master, cm), ("m", m, cv), ("v", v, cp)):
+                err = _norm_rel(dev_t.cpu().numpy(), ref)
+                worst[f"{name}@{step}"] = err
+                assert err <= rtol, (name, step, err)
+            assert torch.equal(p.view(torch.int16), master.to(torch.bfloat16).view(torch.int16))
+    print("fast-mode norm-relative errors", worst)
 
 
 def test_adamw_with_clip_coef(oracle, native):

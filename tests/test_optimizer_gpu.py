@@ -246,3 +246,30 @@ def test_grad_delivery_errors_and_no_sync(native):
     assert torch.equal(acc.param_buffer, ref.param_buffer)
     ref.close()
     acc.close()
+
+
+@pytest.mark.parametrize("clip", [None, 1.0])
+def test_fast_adamw_single_rank_within_tolerance(oracle, native, clip):
+    """adamw='fast' on the d = 1 fused pack+AdamW path: master within 1e-6
+    norm-relative of the exact oracle after step 1, 1e-5 after step 3."""
+    gs = config_gradset("odd")
+    p0 = init_params(gs, DEV)
+    opt = DistributedOptimizer(p0, bucket_size=100_000, clip=clip, adamw="fast")
+    L = opt.layout
+    state = _oracle_state(oracle, L, [p.cpu().numpy() for p in p0])
+    for step in (1, 2, 3):
+        grads = make_grads(gs, step, 0, DEV)
+        opt.step(grads)
+        torch.cuda.synchronize()
+        oracle.step_all_ranks([[u16(g) for g in grads]], [
+            {"params": [(s.index, s.offset, s.numel) for s in b.slots], "numel": b.numel}
+            for b in L.buckets], state, step, opt.lr, opt.betas, opt.eps, opt.weight_decay, clip=clip)
+        rtol = 1e-6 if step == 1 else 1e-5
+        for bi, b in enumerate(L.buckets):
+            off = L.shard_offsets()[bi]
+            got = opt.master[off:off + b.numel].cpu().numpy().astype(np.float64)
+            want = state[bi][0][0]
+            assert np.abs(got - want).max() / np.abs(want).max() <= rtol
+            assert torch.equal(opt.param_buffer[b.start:b.start + b.numel].view(torch.int16),
+                               opt.master[off:off + b.numel].to(torch.bfloat16).view(torch.int16))
+    opt.close()

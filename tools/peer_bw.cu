@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 struct Peers { const uint8_t* p[8]; };
 
 template <int VEC, int U>
@@ -174,5 +176,110 @@ extern "C" int nvls_bw_run(void* mc, int64_t off, int64_t off2, int64_t bytes, v
     else if (what == 2) nvls_launch<8, 2>(m, off, off2, bytes, o, unroll, grid, s);
     else nvls_launch<8, 3>(m, off, off2, bytes, o, unroll, grid, s);
   }
+  return static_cast<int>(cudaGetLastError());
+}
+
+// ---------------------------------------------------------------------------
+// TMA modes: one elected thread per CTA moves whole tiles with the bulk-copy
+// engine (cp.async.bulk) from the d peers' buffers into a STAGES-deep
+// shared-memory ring (mbarrier complete_tx); the CTA's threads XOR-fold the d
+// tiles (the reduce-scatter's read pattern) and, for "both", bulk-store the
+// folded tile to every peer's second region (the all-gather's write pattern).
+// Bytes in flight per CTA = STAGES * d * tile, independent of registers.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile("{\n.reg .pred done;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 done, [%0], %1;\n@!done bra W_%=;\n}\n"
+               ::"r"(su32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(su32(src)), "r"(bytes)
+               : "memory");
+}
+
+template <int STAGES, bool BOTH>
+__global__ void __launch_bounds__(256) tma_kernel(Peers ps, int d, int64_t off, int64_t off2, int64_t bytes,
+                                                  int tile, uint8_t* out) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* in = smem;                                        // [STAGES][d][tile]
+  uint8_t* red = smem + static_cast<int64_t>(STAGES) * d * tile;   // [STAGES][tile] (BOTH)
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + (BOTH ? STAGES * tile : 0));
+  const int64_t n_tiles = bytes / tile;
+  const int64_t mine = (n_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) mb_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t i) {
+    const int s = static_cast<int>(i % STAGES);
+    const int64_t t = blockIdx.x + i * gridDim.x;
+    mb_expect(&full[s], static_cast<uint32_t>(d * tile));
+    for (int q = 0; q < d; ++q)
+      g2s(in + (static_cast<int64_t>(s) * d + q) * tile, ps.p[q] + off + t * tile, tile, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < mine && i < STAGES; ++i) issue(i);
+  uint32_t acc = 0;
+  for (int64_t i = 0; i < mine; ++i) {
+    const int s = static_cast<int>(i % STAGES);
+    if (BOTH && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(STAGES - 1) : "memory");
+    mb_wait(&full[s], static_cast<uint32_t>((i / STAGES) & 1));
+    const uint4* src = reinterpret_cast<const uint4*>(in + static_cast<int64_t>(s) * d * tile);
+    const int words = tile / 16;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) {
+      uint4 x = src[w];
+      for (int q = 1; q < d; ++q) {
+        const uint4 y = src[q * words + w];
+        x.x ^= y.x; x.y ^= y.y; x.z ^= y.z; x.w ^= y.w;
+      }
+      if (BOTH) reinterpret_cast<uint4*>(red + static_cast<int64_t>(s) * tile)[w] = x;
+      else acc ^= x.x ^ x.w;
+    }
+    if (BOTH) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (BOTH) {
+        const int64_t t = blockIdx.x + i * gridDim.x;
+        for (int q = 0; q < d; ++q)
+          s2g(const_cast<uint8_t*>(ps.p[q]) + off2 + t * tile, red + static_cast<int64_t>(s) * tile, tile);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      if (i + STAGES < mine) issue(i + STAGES);
+    }
+  }
+  if (BOTH && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  if (acc == 0x12345678u) out[0] = 1;
+}
+
+// mode 6 = tma read, 7 = tma both; `vec` carries the tile bytes per peer, `unroll` the stages
+extern "C" int tma_bw_run(const void* const* ptrs, int d, int64_t off, int64_t bytes, void* out, int mode,
+                          int tile, int stages, int grid, void* stream) {
+  Peers ps{};
+  for (int q = 0; q < d && q < 8; ++q) ps.p[q] = static_cast<const uint8_t*>(ptrs[q]);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint8_t* o = static_cast<uint8_t*>(out);
+  const bool both = mode == 7;
+  const int smem = stages * d * tile + (both ? stages * tile : 0) + stages * 8;
+#define TMA_L(ST, B)                                                                                  \
+  do {                                                                                                \
+    cudaFuncSetAttribute(tma_kernel<ST, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);      \
+    tma_kernel<ST, B><<<grid, 256, smem, s>>>(ps, d, off, off + d * bytes, bytes, tile, o);           \
+  } while (0)
+  if (stages == 2) { if (both) TMA_L(2, true); else TMA_L(2, false); }
+  else if (stages == 3) { if (both) TMA_L(3, true); else TMA_L(3, false); }
+  else { if (both) TMA_L(4, true); else TMA_L(4, false); }
+#undef TMA_L
   return static_cast<int>(cudaGetLastError());
 }
