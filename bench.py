@@ -290,6 +290,8 @@ def parity_probe(opt, gs, rank: int, dev, gdtype, world: int) -> dict:
         exact = opt.backend in ("p2p", "none")
         out["reduce_scatter_rule"] = ("bit-exact rank-order fp32 sum" if exact
                                       else "within d/2 bf16 ulp of sum|x| (switch / ring order)")
+        out["adamw_rule"] = ("bit-exact" if opt.adamw_mode == "exact"
+                             else "fast mode: within 1e-6 norm-relative, params = RNE(master)")
         step = opt.step_count
         checked = 0
         for bi in sample:
@@ -313,9 +315,17 @@ def parity_probe(opt, gs, rank: int, dev, gdtype, world: int) -> dict:
             want_p = oracle.adamw(master, m, v, dev_red, step, opt.lr, opt.betas, opt.eps, opt.weight_decay,
                                   coef=coef)
             o, n = offs[bi], hi - lo
+            fast = opt.adamw_mode == "fast"
             for name, want, got in (("master", master, opt.master), ("m", m, opt.exp_avg), ("v", v, opt.exp_avg_sq)):
-                if not np.array_equal(got[o:o + n].cpu().numpy().view(np.uint32), want.view(np.uint32)):
+                g = got[o:o + n].cpu().numpy()
+                if fast:    # one step from the same state: north-star 1e-6, norm-relative
+                    err = float(np.abs(g.astype(np.float64) - want).max() / max(np.abs(want).max(), 1e-30))
+                    out.setdefault("max_norm_rel_err", {})[name] = max(err, out.get("max_norm_rel_err", {}).get(name, 0))
+                    if err > 1e-6:
+                        errors.append(f"bucket {bi}: {name} rel err {err:.2e}")
+                elif not np.array_equal(g.view(np.uint32), want.view(np.uint32)):
                     errors.append(f"bucket {bi}: {name}")
+            want_p = u16(opt.master[o:o + n].to(torch.bfloat16)) if fast else want_p
             if not np.array_equal(u16(opt.param_buffer[lo:hi]), want_p):
                 errors.append(f"bucket {bi}: gathered params")
             checked += n
@@ -474,7 +484,7 @@ def north_star_probe(args, world: int, rank: int, dev) -> dict:
 
     gs = config_gradset("llama7b")
     p0 = init_params(gs, dev)
-    opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=1.0,
+    opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=1.0, adamw=args.adamw,
                                dp_group=DPGroup(tuple(range(world)), rank), span_numel=args.span_numel)
     del p0
     torch.cuda.empty_cache()
@@ -538,7 +548,8 @@ def scenario_probe(args, path: Path, world: int, rank: int, dev) -> dict:
     sr = setup_rank(scenario, rank)
     gs = sr.gradset
     p0 = init_params(gs, dev)
-    opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=1.0, span_numel=args.span_numel)
+    opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=1.0, span_numel=args.span_numel,
+                         adamw=args.adamw)
     del p0
     torch.cuda.empty_cache()
     grads = make_grads(gs, 1, rank, dev)
@@ -641,7 +652,7 @@ def run_ours(args) -> None:
         gs = sr.gradset
         clip = 1.0 if args.clip is None else (None if args.clip <= 0 else args.clip)
         p0 = init_params(gs, dev)
-        opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=clip, backend=args.backend,
+        opt = make_optimizer(sr, p0, bucket_size=args.bucket_size, clip=clip, backend=args.backend, adamw=args.adamw,
                              span_numel=args.span_numel)
         stage_params = {sr.placement.stage: gs.total}
         gathered = [None] * world
@@ -658,7 +669,7 @@ def run_ours(args) -> None:
         gs = config_gradset(args.config)
         p0 = init_params(gs, dev)
         group = DPGroup(tuple(range(world)), rank)
-        opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group,
+        opt = DistributedOptimizer(p0, bucket_size=args.bucket_size, clip=clip, dp_group=group, adamw=args.adamw,
                                    backend=args.backend, span_numel=args.span_numel,
                                    first_span_numel=args.first_span_numel,
                                    param_barriers=bool(args.param_barriers))
@@ -847,7 +858,7 @@ def run_ours(args) -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16-grads/f32-adamw", "data": "synthetic",
             "config": _config_doc(args, clip, params_per_step, opt_info["buckets"], opt_info["dp"], scen),
-            "backend": opt_info["backend"], "parity": parity,
+            "backend": opt_info["backend"], "adamw": args.adamw, "parity": parity,
             "roofline": roof, "step_roofline": step_roof, "kernels": kernels,
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk, "gpu_launches": launches,
             "overlap": overlap, "extras": extras,
@@ -880,6 +891,8 @@ def main():
                     help="p2p/nvls, hook-driven flows (the overlap measurement): params-ready barrier per "
                          "span (1) or one end-of-step barrier (0); step() always ends with one barrier")
     ap.add_argument("--backend", default="auto")
+    ap.add_argument("--adamw", default="exact", choices=["exact", "fast"],
+                    help="AdamW arithmetic: exact (bit-exact vs the oracle) or fast (FMA + MUFU, within 1e-6/1e-5)")
     ap.add_argument("--clip", type=float, default=None, help="override clip (<=0 disables)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -68,13 +68,18 @@ class SymmetricTensor:
 
 
 def group_for(ranks, world_group_ranks=None):
-    """Process group over ``ranks`` (WORLD when it spans everybody).
+    """Process group over ``ranks``: the WORLD when it spans everybody.
 
-    ``dist.new_group`` is collective over the WORLD: callers that need several
-    disjoint DP rows (config 4) should build them with
-    ``dist.new_subgroups_by_enumeration`` on every rank instead and pass the
-    row's group explicitly."""
+    Any other member set needs a group that every rank of the world created
+    in the same call (``dist.new_group`` is collective over the WORLD and
+    must see identical arguments everywhere): build all DP rows at once with
+    ``dist.new_subgroups_by_enumeration`` (``scenario_run.setup_rank`` does)
+    and pass the row's group as ``process_group`` / ``norm_group``."""
+    from .errors import InfeasibleConfigError
+
     ranks = tuple(ranks)
     if len(ranks) == dist.get_world_size() and sorted(ranks) == list(range(len(ranks))):
         return dist.group.WORLD
-    return dist.new_group(list(ranks))
+    raise InfeasibleConfigError(
+        f"ranks {ranks} are not the whole world: pass the row's process group (create every row on every "
+        "rank with dist.new_subgroups_by_enumeration, e.g. scenario_run.setup_rank)")

@@ -202,6 +202,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=8192, help="micro-batch tokens per GPU (b*s)")
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--backend", default="auto")
+    ap.add_argument("--adamw", default="exact", choices=["exact", "fast"])
     ap.add_argument("--clip", type=float, default=0.0)
     ap.add_argument("--bucket-size", type=int, default=25_000_000)
     ap.add_argument("--sm-budget", type=int, default=0,
@@ -220,7 +221,7 @@ def main():
     dev = torch.device("cuda", local)
     gs = config_gradset(a.config)
     p0 = init_params(gs, dev)
-    opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None,
+    opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None, adamw=a.adamw,
                                dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
                                sm_budget=a.sm_budget or None,
                                pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier),
