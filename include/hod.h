@@ -93,9 +93,13 @@ const char* hod_last_error(void);
 long long hod_launch_count(void);
 /* Cap every subsequent launch of the process (all threads: autograd issues
  * hook-driven launches from its own device thread) at `max_ctas` CTAs
- * (0 = no cap).  The overlapped optimizer sets it while backward GEMMs run so
- * its kernels occupy a bounded slice of the 148 SMs (pair with cuBLAS's SM
- * carve-out); partial-sum kernels use min(cap, HOD_SUMSQ_PARTIALS) CTAs and
+ * (0 = no cap).  The overlapped optimizer sets it while backward GEMMs run.
+ * A cap <= 148 (one CTA per SM) is the CO-RESIDENT mode: the launchers also
+ * pick register-light kernel variants, so that every optimizer CTA fits on an
+ * SM beside a resident cuBLAS GEMM CTA and the two share the SM (tensor
+ * cores vs HBM/NVLink) instead of time-slicing it.  Every kernel prefers the
+ * maximum shared-memory carveout for the same reason (HOD_CARVEOUT=0 turns
+ * that off).  Partial-sum kernels use min(cap, HOD_SUMSQ_PARTIALS) CTAs and
  * zero the unused partial slots. */
 int hod_set_grid_limit(int max_ctas);
 

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/hod.h"
 
 namespace hod {
@@ -169,8 +171,25 @@ __device__ __forceinline__ void adamw_elem(float& p, float& m, float& v, float g
 }
 
 // CTA cap set by hod_set_grid_limit (0 = none): lets the optimizer's kernels
-// co-run with the backward GEMMs on a bounded slice of the SMs.
+// co-run with the backward GEMMs.  A cap of at most one CTA per SM is the
+// CO-RESIDENT mode: launchers then also pick their register-light variants so
+// that one optimizer CTA (256 threads, <= 88 registers, no shared memory)
+// fits beside a resident cuBLAS GEMM CTA (measured nvjet sm_100 kernels: 256
+// threads x 168 registers, 213 KB shared memory, tools/corun_probe.py).
 int grid_limit();
+inline bool coresident() { return grid_limit() > 0 && grid_limit() <= kSMs; }
+
+// Co-resident launches prefer the maximum shared-memory carveout.  An SM runs
+// CTAs of one L1/shared split at a time: a kernel launched with the default
+// (small) carveout keeps the SMs it occupies in that configuration, and a
+// GEMM that needs 213 KB of shared memory cannot be placed there until they
+// drain — the optimizer would then serialise with backward instead of
+// sharing the SMs.  Measured (tools/corun_probe.py, profiles/r02_corun.jsonl):
+// AdamW at one CTA/SM launched BEFORE a GEMM loop hides 0.72 of its time with
+// the carveout vs 0.0 without.  Full-GPU launches keep the default split: the
+// larger L1 holds more loads in flight (AdamW alone 6.3 vs 5.3 TB/s).
+// HOD_CARVEOUT=0 disables it (A/B runs).
+bool carveout_enabled();
 
 // HOD_CTAS_PER_SM (env) overrides the per-kernel CTAs-per-SM cap (tuning runs).
 int ctas_per_sm_override();
@@ -195,12 +214,35 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, c
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = 0;
+  if (pdl_enabled()) cfg.numAttrs = 1;
+  if (coresident() && carveout_enabled()) {
+    attr[cfg.numAttrs].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+    attr[cfg.numAttrs].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+    ++cfg.numAttrs;
+  }
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<Args&&>(args)...);
+}
+
+// <<<grid, block, smem, stream>>> with the co-resident carveout applied.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePreferredSharedMemoryCarveout;
+  attr[0].val.sharedMemCarveout = cudaSharedmemCarveoutMaxShared;
+  cfg.attrs = attr;
+  cfg.numAttrs = (coresident() && carveout_enabled()) ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 inline int grid_for(int64_t work_items, int per_block, int max_blocks_per_sm = 8) {

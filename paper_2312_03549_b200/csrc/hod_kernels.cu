@@ -35,6 +35,14 @@ bool pdl_enabled() {
   return v;
 }
 
+bool carveout_enabled() {
+  static const bool v = [] {
+    const char* e = getenv("HOD_CARVEOUT");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+
 int ctas_per_sm_override() {
   static const int v = [] {
     const char* e = getenv("HOD_CTAS_PER_SM");
@@ -284,7 +292,7 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
       const int grid = grid_for(n_vec * 32, kThreads, 2);
       count_launch(1);
 #define HOD_AV(CLIP, FAST) \
-      adamw_vec_kernel<GradT, CLIP, FAST><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef)
+      launch(adamw_vec_kernel<GradT, CLIP, FAST>, grid, kThreads, 0, s, master, exp_avg, exp_avg_sq, grad, param, n_vec, c, clip_coef)
       if (clip_coef) { if (c.fast) HOD_AV(true, true); else HOD_AV(true, false); }
       else { if (c.fast) HOD_AV(false, true); else HOD_AV(false, false); }
 #undef HOD_AV
@@ -295,7 +303,7 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
     const int grid = grid_for(n - done, kThreads);
     count_launch(1);
 #define HOD_AS(CLIP, FAST) \
-    adamw_scalar_kernel<GradT, CLIP, FAST><<<grid, kThreads, 0, s>>>(master, exp_avg, exp_avg_sq, grad, param, done, n, c, clip_coef)
+    launch(adamw_scalar_kernel<GradT, CLIP, FAST>, grid, kThreads, 0, s, master, exp_avg, exp_avg_sq, grad, param, done, n, c, clip_coef)
     if (clip_coef) { if (c.fast) HOD_AS(true, true); else HOD_AS(true, false); }
     else { if (c.fast) HOD_AS(false, true); else HOD_AS(false, false); }
 #undef HOD_AS
@@ -602,9 +610,9 @@ int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_
       else
         launch_pdl(pack_sumsq_kernel<float>, grid, kSumsqThreads, s, t, span, scale, partials, 0);
     } else if (src_dtype == HOD_DTYPE_BF16) {
-      pack_sumsq_kernel<uint16_t><<<grid, kSumsqThreads, 0, s>>>(t, span, scale, partials, 1);
+      launch(pack_sumsq_kernel<uint16_t>, grid, kSumsqThreads, 0, s, t, span, scale, partials, 1);
     } else {
-      pack_sumsq_kernel<float><<<grid, kSumsqThreads, 0, s>>>(t, span, scale, partials, 1);
+      launch(pack_sumsq_kernel<float>, grid, kSumsqThreads, 0, s, t, span, scale, partials, 1);
     }
     (void)lo;
     return cuda_status(cudaGetLastError(), "hod_pack_sumsq launch");
@@ -614,7 +622,7 @@ int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_
 int hod_sumsq_bf16(const uint16_t* x, int64_t n, float* partials, void* stream) {
   if (!partials || n < 0 || (n > 0 && !x)) { set_error("hod_sumsq_bf16: bad arguments"); return HOD_EINVAL; }
   count_launch(1);
-  sumsq_kernel<<<partials_grid(), kSumsqThreads, 0, static_cast<cudaStream_t>(stream)>>>(x, n, aligned16(x), partials);
+  launch(sumsq_kernel, partials_grid(), kSumsqThreads, 0, static_cast<cudaStream_t>(stream), x, n, aligned16(x), partials);
   return cuda_status(cudaGetLastError(), "hod_sumsq_bf16 launch");
 }
 
@@ -626,8 +634,8 @@ int hod_sumsq(const uint16_t* x, int64_t n, float* out, void* stream) {
   if (rc) return rc;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   count_launch(2);
-  sumsq_kernel<<<partials_grid(), kSumsqThreads, 0, s>>>(x, n, aligned16(x), scratch);
-  accumulate_partials_kernel<<<1, 32, 0, s>>>(scratch, HOD_SUMSQ_PARTIALS, out);
+  launch(sumsq_kernel, partials_grid(), kSumsqThreads, 0, s, x, n, aligned16(x), scratch);
+  launch(accumulate_partials_kernel, 1, 32, 0, s, scratch, HOD_SUMSQ_PARTIALS, out);
   return cuda_status(cudaGetLastError(), "hod_sumsq launch");
 }
 
@@ -641,14 +649,14 @@ int hod_adamw(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* 
 int hod_sum_partials(const float* partials, int64_t n_partials, float* out, void* stream) {
   if (!partials || !out || n_partials < 0) { set_error("hod_sum_partials: bad arguments"); return HOD_EINVAL; }
   count_launch(1);
-  sum_partials_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(partials, n_partials, out);
+  launch(sum_partials_kernel, 1, 32, 0, static_cast<cudaStream_t>(stream), partials, n_partials, out);
   return cuda_status(cudaGetLastError(), "hod_sum_partials launch");
 }
 
 int hod_clip_coef(const float* sumsq, float max_norm, float* coef, float* norm, void* stream) {
   if (!sumsq || !coef || !(max_norm > 0.0f)) { set_error("hod_clip_coef: bad arguments"); return HOD_EINVAL; }
   count_launch(1);
-  clip_coef_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(sumsq, max_norm, coef, norm);
+  launch(clip_coef_kernel, 1, 1, 0, static_cast<cudaStream_t>(stream), sumsq, max_norm, coef, norm);
   return cuda_status(cudaGetLastError(), "hod_clip_coef launch");
 }
 

@@ -484,8 +484,8 @@ template <int D, int kSrc, int kMode, int U, int W>
 static void launch_u_w(const SpanArgs& a, const BarrierArgs& b, const AdamWConsts& c, int rank, int grid,
                        cudaStream_t s) {
   // the RS half has no update: only the exact instantiation exists
-  if (kMode != 1 && c.fast) p2p_step_kernel<D, kSrc, kMode, U, W, kMode != 1><<<grid, kThreads, 0, s>>>(a, b, c, rank);
-  else p2p_step_kernel<D, kSrc, kMode, U, W, false><<<grid, kThreads, 0, s>>>(a, b, c, rank);
+  if (kMode != 1 && c.fast) launch(p2p_step_kernel<D, kSrc, kMode, U, W, kMode != 1>, grid, kThreads, 0, s, a, b, c, rank);
+  else launch(p2p_step_kernel<D, kSrc, kMode, U, W, false>, grid, kThreads, 0, s, a, b, c, rank);
 }
 
 template <int D, int kSrc, int kMode>
@@ -493,9 +493,11 @@ static void launch_step(const SpanArgs& a, const BarrierArgs& b, const AdamWCons
                         int grid, cudaStream_t s) {
   count_launch(1);
   // measured (tools/p2p_microbench.py): two items in flight per thread pay off
-  // at d = 2 (one remote load each); at d >= 4 the register cost outweighs it
+  // at d = 2 (one remote load each); at d >= 4 the register cost outweighs it.
+  // Co-resident launches (beside backward GEMMs) take the one-item variant:
+  // <= 84 registers, so a CTA fits the 22.5 K registers a GEMM CTA leaves.
   const int u = unroll_setting();
-  const bool two = u >= 2 || (u == 0 && D == 2);
+  const bool two = !coresident() && (u >= 2 || (u == 0 && D == 2));
   const int w = wide_setting();
   if (kSrc == kSrcPeer && kMode != 2 && (w > 0 || (w < 0 && D == 2))) {
     if (two) launch_u_w<D, kSrc, kMode, 2, 1>(a, b, c, rank, grid, s);
@@ -621,7 +623,7 @@ int hod_p2p_step(const hod_p2p_span* sp, int mode, const hod_adamw_params* hp, v
 int hod_p2p_signal(uint32_t* peer_flag, uint32_t epoch, void* stream) {
   if (!peer_flag) { set_error("hod_p2p_signal: null flag"); return HOD_EINVAL; }
   count_launch(1);
-  signal_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(peer_flag, epoch);
+  launch(signal_kernel, 1, 1, 0, static_cast<cudaStream_t>(stream), peer_flag, epoch);
   return cuda_status(cudaGetLastError(), "hod_p2p_signal launch");
 }
 
@@ -629,8 +631,8 @@ int hod_p2p_wait(const uint32_t* flag, uint32_t epoch, unsigned long long timeou
                  void* stream) {
   if (!flag) { set_error("hod_p2p_wait: null flag"); return HOD_EINVAL; }
   count_launch(1);
-  wait_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(flag, epoch,
-                                                             timeout_ns ? timeout_ns : 20000000000ull, err);
+  launch(wait_kernel, 1, 1, 0, static_cast<cudaStream_t>(stream), flag, epoch,
+         timeout_ns ? timeout_ns : 20000000000ull, err);
   return cuda_status(cudaGetLastError(), "hod_p2p_wait launch");
 }
 
@@ -643,7 +645,7 @@ int hod_p2p_barrier(uint64_t* const* flags, int d, int rank, int slot, uint32_t 
   int rc = fill_barrier(flags, d, rank, slot, epoch, tag, timeout_ns, err, &b);
   if (rc) return rc;
   count_launch(1);
-  barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(b, d, rank);
+  launch(barrier_kernel, 1, 32, 0, static_cast<cudaStream_t>(stream), b, d, rank);
   return cuda_status(cudaGetLastError(), "hod_p2p_barrier launch");
 }
 
@@ -661,7 +663,7 @@ int hod_p2p_norm(const float* partials, int64_t n_partials, double* const* xchg,
   int rc = fill_barrier(flags, d, rank, slot, epoch, HOD_NORM_TAG, timeout_ns, err, &b);
   if (rc) return rc;
   count_launch(1);
-  norm_exchange_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(
+  launch(norm_exchange_kernel, 1, 32, 0, static_cast<cudaStream_t>(stream), 
       partials, n_partials, x, xchg[rank], b, d, rank, max_norm, coef, norm, sumsq);
   return cuda_status(cudaGetLastError(), "hod_p2p_norm launch");
 }

@@ -51,6 +51,7 @@ _PDL = os.environ.get("HOD_PDL", "1") != "0"
 
 _BF16 = torch.bfloat16
 BACKENDS = ("none", "nccl", "p2p", "nvls")
+_CORESIDENT_CTAS = 148       # one CTA per SM (include/hod.h hod_set_grid_limit)
 _SPAN_MAX_BUCKETS = 0xFFFF   # bucket indices fit the 16-bit halves of a span tag
 
 
@@ -194,9 +195,17 @@ class DistributedOptimizer:
             raise InfeasibleConfigError(f"{backend} supports at most {nat.HOD_P2P_MAX_RANKS} ranks")
         self.backend = backend
         self.keep_reduced = keep_reduced
-        # CTAs per launch while backward still runs (None = whole GPU); the last
-        # bucket and the post-backward phase always get the whole GPU
-        self.sm_budget = sm_budget
+        # CTAs per launch while backward still runs; the last bucket, step()
+        # and the post-backward phase always get the whole GPU.  None (auto):
+        # 148 = one CTA per SM, the CO-RESIDENT mode of hod_set_grid_limit —
+        # each optimizer CTA fits beside a resident cuBLAS GEMM CTA and shares
+        # its SM (HBM/NVLink vs tensor cores) instead of time-slicing it
+        # (tools/corun_probe.py: 0.55-0.72 of a co-resident update hidden,
+        # ~0 with full-GPU grids).  0 = whole GPU; env HOD_SM_BUDGET overrides.
+        env = os.environ.get("HOD_SM_BUDGET")
+        if env is not None:
+            sm_budget = int(env)
+        self.sm_budget = _CORESIDENT_CTAS if sm_budget is None else int(sm_budget)
         # p2p/nvls: consecutive packed buckets are coalesced into one fused
         # launch until the span holds >= span_numel elements (1 = per bucket)
         self.span_numel = int(span_numel)
@@ -653,7 +662,8 @@ class DistributedOptimizer:
     def _launch_bucket(self, bi: int) -> None:
         last = sum(self._launched) == len(self._launched) - 1
         base = nat.grid_base()
-        if last or not self.sm_budget:
+        # step(): no backward to share the SMs with
+        if last or not self.sm_budget or self._whole_step:
             self._launch_bucket_body(bi)
             return
         nat.call("hod_set_grid_limit", min(int(self.sm_budget), base) if base else int(self.sm_budget))

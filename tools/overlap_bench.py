@@ -35,7 +35,7 @@ from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
 from paper_2312_03549_b200.synthetic import init_params  # noqa: E402
 
 
-def measure(opt, gs, tokens: int, iters: int, world: int, dev, sm_budget: int = 0) -> dict:
+def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: int = 0) -> dict:
     """Backward-only and full-iteration exposure of ``opt`` with a synthetic
     cuBLAS GEMM forward/backward of ``tokens`` tokens per GPU (see module doc)."""
     T = tokens
@@ -112,13 +112,13 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, sm_budget: int = 
             ms = float(t.item())
         return ms
 
-    if sm_budget:
+    if gemm_carveout:
         # the SM carve-out is honoured by the cuBLASLt path
         torch.backends.cuda.preferred_blas_library("cublaslt")
 
     def carve(on: bool):
-        if sm_budget and hasattr(torch._C, "_set_sm_carveout_experimental"):
-            torch._C._set_sm_carveout_experimental(sm_budget if on else None)
+        if gemm_carveout and hasattr(torch._C, "_set_sm_carveout_experimental"):
+            torch._C._set_sm_carveout_experimental(gemm_carveout if on else None)
 
     def backward_carved():
         carve(True)
@@ -137,7 +137,7 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, sm_budget: int = 
         opt.step(grads)
         overlapped()
     t_bwd = timed(lambda: backward(False))
-    t_bwd_carved = timed(backward_carved) if sm_budget else t_bwd
+    t_bwd_carved = timed(backward_carved) if gemm_carveout else t_bwd
     t_opt = timed(lambda: opt.step(grads))
     t_ovl = timed(overlapped)
     for _ in range(2):
@@ -174,7 +174,7 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, sm_budget: int = 
                 and "embed" not in t.name)
     doc = {"world": world, "backend": opt.backend, "tokens_per_gpu": T,
            "pre_barrier": opt.pre_barrier, "span_numel": opt.span_numel,
-           "sm_budget": sm_budget,
+           "sm_budget": opt.sm_budget, "gemm_carveout": gemm_carveout,
            "clip": opt.clip, "buckets": len(opt.layout.buckets),
            "t_backward_ms": round(t_bwd, 3), "t_backward_carved_ms": round(t_bwd_carved, 3),
            "t_optimizer_alone_ms": round(t_opt, 3),
@@ -205,9 +205,11 @@ def main():
     ap.add_argument("--adamw", default="exact", choices=["exact", "fast"])
     ap.add_argument("--clip", type=float, default=0.0)
     ap.add_argument("--bucket-size", type=int, default=25_000_000)
-    ap.add_argument("--sm-budget", type=int, default=0,
-                    help="CTAs per optimizer launch during backward; the backward GEMMs get the "
-                         "same number of SMs carved out (torch._C._set_sm_carveout_experimental)")
+    ap.add_argument("--sm-budget", type=int, default=None,
+                    help="CTAs per optimizer launch during backward (default: the optimizer's "
+                         "co-resident 148; 0 = whole GPU)")
+    ap.add_argument("--gemm-carveout", type=int, default=0,
+                    help="SMs withheld from the backward GEMMs (torch._C._set_sm_carveout_experimental)")
     ap.add_argument("--pre-barrier", type=int, default=None,
                     help="1: arrival barrier as a 1-CTA kernel before each span (optimizer pre_barrier)")
     ap.add_argument("--span-numel", type=int, default=None, help="fused-launch span threshold (elements)")
@@ -223,11 +225,11 @@ def main():
     p0 = init_params(gs, dev)
     opt = DistributedOptimizer(p0, bucket_size=a.bucket_size, clip=a.clip if a.clip > 0 else None, adamw=a.adamw,
                                dp_group=DPGroup(tuple(range(world)), rank), backend=a.backend,
-                               sm_budget=a.sm_budget or None,
+                               sm_budget=a.sm_budget,
                                pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier),
                                **({"span_numel": a.span_numel} if a.span_numel else {}))
     del p0
-    doc = measure(opt, gs, a.tokens, a.iters, world, dev, sm_budget=a.sm_budget)
+    doc = measure(opt, gs, a.tokens, a.iters, world, dev, gemm_carveout=a.gemm_carveout)
     doc.update({"config": a.config, "bucket_size": a.bucket_size})
     if rank == 0:
         print(json.dumps(doc))
