@@ -505,9 +505,7 @@ def north_star_probe(args, world: int, rank: int, dev) -> dict:
     sys.path.insert(0, str(ROOT / "tools"))
     from overlap_bench import measure
 
-    opt.pre_barrier = True   # the hook-driven default (register_hooks)
     o = measure(opt, gs, args.overlap_tokens, 3, world, dev)
-    opt.pre_barrier = False
     parity = None if args.no_parity else parity_probe(opt, gs, rank, dev, torch.bfloat16, world)
     P, d = gs.total, world
     peak, _ = _peaks()
@@ -817,7 +815,6 @@ def run_ours(args) -> None:
         sys.path.insert(0, str(ROOT / "tools"))
         from overlap_bench import measure
 
-        opt.pre_barrier = True   # the hook-driven default (register_hooks)
         o = measure(opt, gs, args.overlap_tokens, 5, world, dev)
         overlap = {"tokens_per_gpu": args.overlap_tokens, "exposed_frac_iteration": o["iteration"]["exposed_frac"],
                    "t_fwd_bwd_ms": o["iteration"]["t_fwd_bwd_ms"],

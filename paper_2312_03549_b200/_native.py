@@ -9,11 +9,13 @@ else on the CPU.
 from __future__ import annotations
 
 import ctypes
+import os
 from pathlib import Path
 
 from .errors import DeviceError
 
-LIB_PATH = Path(__file__).resolve().parent / "libhod.so"
+# HOD_LIB: an alternative build of the same library (A/B tuning runs only)
+LIB_PATH = Path(os.environ.get("HOD_LIB", Path(__file__).resolve().parent / "libhod.so"))
 
 HOD_PACK_MAX_ENTRIES = 64
 HOD_SUMSQ_PARTIALS = 296

@@ -44,8 +44,11 @@ def _stale() -> bool:
     return any(d.exists() and d.stat().st_mtime > mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None, defines=()) -> Path:
+    """Build libhod.so (``out``/``defines``: an A/B variant, e.g.
+    ``-DHOD_STREAM_HINTS=0`` into another file, loaded with HOD_LIB)."""
+    target = Path(out) if out else LIB
+    if not force and not out and not _stale():
         return LIB
     inc, lib = _nccl_dirs()
     srcs = [str(CSRC / s) for s in SOURCES if (CSRC / s).exists()]
@@ -55,25 +58,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         "-Xptxas", "-v" if verbose else "-O3",
         f"-I{inc}", f"-I{ROOT / 'include'}",
         *os.environ.get("HOD_NVCC_EXTRA", "").split(),   # tuning builds, e.g. -DHOD_P2P_MINB=3
+        *defines,
         *srcs,
         f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath,{lib}",
-        "-o", str(LIB),
+        "-o", str(target),
     ]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = target.with_suffix(".so.tmp")
     cmd[-1] = str(tmp)
     subprocess.run(cmd, check=True)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--out", default=None, help="A/B variant output path")
+    ap.add_argument("-D", dest="defines", action="append", default=[], help="extra -D define (A/B variant)")
     a = ap.parse_args()
-    print(build(force=a.force, verbose=a.verbose))
+    print(build(force=a.force, verbose=a.verbose, out=a.out, defines=[f"-D{x}" for x in a.defines]))
 
 
 if __name__ == "__main__":

@@ -228,14 +228,14 @@ class DistributedOptimizer:
         # share of a training iteration drops at d = 2 14.1 -> 12.8 % (1.3B),
         # 11.3 -> 9.7 % (LLaMA-7B clip), at d = 4 10.5 -> 9.4 % and 7.4 ->
         # 6.2 %, but the standalone step pays ~20 us per span (LLaMA-7B
-        # d = 4: 34.7 -> 35.4 ms).  Default (None): on once the optimizer is
-        # driven by autograd hooks (register_hooks: backward kernels share the
-        # SMs), off for resident-gradient steps; env HOD_PRE_BARRIER=0/1 forces.
+        # d = 4: 34.7 -> 35.4 ms).  Default (None): on for buckets delivered
+        # by grad_ready during backward (hooks: backward kernels share the
+        # SMs), off inside step() (resident gradients); env HOD_PRE_BARRIER=0/1
+        # forces.
         env = os.environ.get("HOD_PRE_BARRIER")
         if env is not None:
             pre_barrier = env == "1"
-        self._pre_barrier_auto = pre_barrier is None
-        self.pre_barrier = bool(pre_barrier)
+        self.pre_barrier = pre_barrier
         self._pending_span: list[int] = []
         self.timeout_ns = int(barrier_timeout_s * 1e9)
         nat.load()
@@ -371,6 +371,9 @@ class DistributedOptimizer:
         self._launched: list[bool] = []
         self._deferred_ag: list[int] = []
         self._in_step = False
+        self._finish_wait = True
+        self._corun_active = False
+        self._ev_span_end = torch.cuda.Event()
         self._sync_enabled = True
 
     # ------------------------------------------------------------------ API
@@ -440,6 +443,7 @@ class DistributedOptimizer:
             if not self._launched[b]:
                 missing = [s.index for s in L.buckets[b].slots if s.index not in self._pending_grads[b]]
                 raise InfeasibleConfigError(f"bucket {b} is missing gradients for params {missing[:8]}")
+        self._finish_wait = wait
         if self.backend in ("p2p", "nvls"):
             self._p2p_finish()
         elif self._deferred_pa:
@@ -571,8 +575,6 @@ class DistributedOptimizer:
         micro-batches run under ``no_sync()`` (the hooks stay silent and the
         gradients accumulate in ``p.grad``); the last micro-batch's backward,
         inside ``begin_step``/``finish_step``, delivers the sums."""
-        if self._pre_barrier_auto:
-            self.pre_barrier = True
         handles = []
         for i, p in enumerate(module_params):
             def hook(param, i=i):
@@ -659,18 +661,32 @@ class DistributedOptimizer:
         lo, hi = b.shard_range(self.shard_index, self.dp)
         return _ptr(self.grad_buffer) + 2 * lo, hi - lo
 
+    def _coresident(self, on: bool):
+        """Context: launches inside it use the co-resident grid (sm_budget)
+        when ``on`` — they share the SMs with the caller's GEMMs."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def ctx():
+            if not on or not self.sm_budget:
+                yield
+                return
+            base = nat.grid_base()
+            nat.call("hod_set_grid_limit", min(int(self.sm_budget), base) if base else int(self.sm_budget))
+            self._corun_active = True
+            try:
+                yield
+            finally:
+                self._corun_active = False
+                nat.call("hod_set_grid_limit", base)
+        return ctx()
+
     def _launch_bucket(self, bi: int) -> None:
         last = sum(self._launched) == len(self._launched) - 1
-        base = nat.grid_base()
-        # step(): no backward to share the SMs with
-        if last or not self.sm_budget or self._whole_step:
+        # step(): no backward to share the SMs with; the last bucket finds
+        # backward (nearly) done
+        with self._coresident(not last and not self._whole_step):
             self._launch_bucket_body(bi)
-            return
-        nat.call("hod_set_grid_limit", min(int(self.sm_budget), base) if base else int(self.sm_budget))
-        try:
-            self._launch_bucket_body(bi)
-        finally:
-            nat.call("hod_set_grid_limit", base)
 
     def _launch_bucket_body(self, bi: int) -> None:
         b = self.layout.buckets[bi]
@@ -837,7 +853,8 @@ class DistributedOptimizer:
         # algorithmic bytes per launch: local HBM (state 24 B + own param 2 B +
         # own grad 2 B per owned element) — NVLink bytes are reported separately
         nbytes = {"fused": 28 * n_total, "rs": 2 * d * n_total + 2 * n_total, "adamw_ag": 28 * n_total}[name]
-        if self.pre_barrier and mode != nat.HOD_P2P_ADAMW_AG:
+        pre = (not self._whole_step) if self.pre_barrier is None else self.pre_barrier
+        if pre and mode != nat.HOD_P2P_ADAMW_AG:
             nat.call("hod_p2p_barrier", self._flag_ptrs(self._sym_flags), d, self.shard_index, sp.slot,
                      sp.epoch, sp.tag, self.timeout_ns, _ptr(self._err), nat.stream_ptr(self.s_comm))
         t0 = self._timed_event(self.s_comm)
@@ -880,6 +897,12 @@ class DistributedOptimizer:
             else:
                 part = _ptr(self._partials) + 4 * nat.HOD_SUMSQ_PARTIALS * pend[0]
                 self._p2p(pend, nat.HOD_P2P_RS, partials=part)
+            if self._corun_active:
+                # co-resident: the next pack starts after this span, so at most
+                # one optimizer CTA sits on an SM — a pack CTA beside a span CTA
+                # would leave too few registers for a GEMM CTA (22.5 K free)
+                self._ev_span_end.record(self.s_comm)
+                self.s_pack.wait_event(self._ev_span_end)
 
     def _p2p_finish(self) -> None:
         nb = len(self.layout.buckets)
@@ -899,9 +922,13 @@ class DistributedOptimizer:
                          _ptr(self._err), ctypes.c_float(self.clip), _ptr(self._coef), _ptr(self._norm),
                          _ptr(self._sumsq), nat.stream_ptr(s))
             # reverse bucket order: the last bucket holds the first layers, which
-            # the next forward needs first
-            for span in reversed(self._spans(range(nb))):
-                self._p2p(span, nat.HOD_P2P_ADAMW_AG, coef_ptr=_ptr(self._coef))
+            # the next forward needs first.  With finish_step(wait=False) the
+            # forward runs concurrently: the first span gets the whole GPU (the
+            # forward waits for it), the others run co-resident beside the
+            # forward GEMMs
+            for k, span in enumerate(reversed(self._spans(range(nb)))):
+                with self._coresident(k > 0 and not self._finish_wait and not self._whole_step):
+                    self._p2p(span, nat.HOD_P2P_ADAMW_AG, coef_ptr=_ptr(self._coef))
                 self._span_done(span)
         else:
             self._queue_p2p(None, final=True)

@@ -174,7 +174,7 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
                 and "embed" not in t.name)
     doc = {"world": world, "backend": opt.backend, "tokens_per_gpu": T,
            "pre_barrier": opt.pre_barrier, "span_numel": opt.span_numel,
-           "sm_budget": opt.sm_budget, "gemm_carveout": gemm_carveout,
+           "sm_budget": opt.sm_budget, "gemm_carveout": gemm_carveout, "adamw": opt.adamw_mode,
            "clip": opt.clip, "buckets": len(opt.layout.buckets),
            "t_backward_ms": round(t_bwd, 3), "t_backward_carved_ms": round(t_bwd_carved, 3),
            "t_optimizer_alone_ms": round(t_opt, 3),
