@@ -153,15 +153,6 @@ int hod_adamw_bf16(float* master, float* exp_avg, float* exp_avg_sq,
                    const uint16_t* grad, uint16_t* param, int64_t n,
                    const hod_adamw_params* hp, const float* clip_coef, void* stream);
 
-/* Same update fed by the Tensor Memory Accelerator: 2048-element chunks are
- * bulk-copied (cp.async.bulk) into a shared-memory ring by one producer thread
- * per CTA and bulk-stored back, so `max_ctas` CTAs (0 = one per SM) stream at
- * HBM speed from few threads — the SM-light variant for overlap with compute.
- * Bit-identical to hod_adamw_bf16. */
-int hod_adamw_tma(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* grad,
-                  uint16_t* param, int64_t n, const hod_adamw_params* hp, const float* clip_coef,
-                  int max_ctas, void* stream);
-
 /* The SURVEY §8b scalar-argument spelling of K2 (same kernel, same bits as
  * hod_adamw_bf16 with hp = {lr, beta1, beta2, eps, weight_decay, step}). */
 int hod_adamw(float* master, float* exp_avg, float* exp_avg_sq, const uint16_t* grad,
@@ -253,11 +244,19 @@ typedef struct hod_p2p_span {
 #define HOD_SPAN_TAG(first, last) ((uint32_t)(first) | ((uint32_t)(last) << 16))
 #define HOD_NORM_TAG 0x4e4f524du /* tag of the norm-exchange barrier */
 
-/* Errors inside a launch go to the device word *err (HOD_ETIMEOUT, HOD_ESPAN).
+/* p2p launches with the whole GPU run the TMA-fed kernel (cp.async.bulk peer
+ * reads / peer writes through a shared-memory ring, one CTA per SM); under a
+ * co-resident grid cap (hod_set_grid_limit <= 148) the register-streaming
+ * kernel, which fits beside a GEMM CTA.  Same results, bit for bit (RS
+ * partial sums: same value within fp32 summation order).  hod_set_span_tma
+ * (initial value: env HOD_SPAN_TMA): 0 = never, 1 = default, 2 = also under
+ * a cap.
+ * Errors inside a launch go to the device word *err (HOD_ETIMEOUT, HOD_ESPAN).
  * Fail-stop: once *err is nonzero every later barrier, span and update launch
  * of this rank returns at entry without signalling its peers (which then time
  * out in turn); the host reads the word and raises. */
 int hod_p2p_step(const hod_p2p_span* span, int mode, const hod_adamw_params* hp, void* stream);
+int hod_set_span_tma(int mode);
 
 /* stand-alone cross-GPU barrier on `slot` (1 CTA): signal (epoch, tag) then wait
  * for all d ranks; a different tag at the same epoch records HOD_ESPAN */

@@ -26,10 +26,10 @@ HOD_DTYPE_F32 = 1
 EXPORTED = (
     "hod_abi_version", "hod_last_error", "hod_launch_count", "hod_set_grid_limit",
     "hod_pack_bf16", "hod_pack_adamw", "hod_pack_sumsq", "hod_sumsq_bf16", "hod_sum_partials", "hod_clip_coef",
-    "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw_tma", "hod_adamw", "hod_sumsq",
+    "hod_adamw_bf16", "hod_adamw_f32", "hod_adamw", "hod_sumsq",
     "hod_nccl_unique_id", "hod_nccl_comm_init", "hod_comm_destroy", "hod_comm_async_error",
     "hod_reduce_scatter_bf16", "hod_all_gather_bf16", "hod_all_reduce_f32",
-    "hod_p2p_step", "hod_p2p_barrier", "hod_p2p_norm", "hod_p2p_signal", "hod_p2p_wait", "hod_ce_copy",
+    "hod_p2p_step", "hod_set_span_tma", "hod_p2p_barrier", "hod_p2p_norm", "hod_p2p_signal", "hod_p2p_wait", "hod_ce_copy",
 )
 
 
@@ -120,7 +120,6 @@ def load(build_if_missing: bool = True):
         "hod_adamw": ([P, P, P, P, P, I64, F, F, F, F, F, I64, P, P], I),
         "hod_sumsq": ([P, I64, P, P], I),
         "hod_adamw_f32": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, P], I),
-        "hod_adamw_tma": ([P, P, P, P, P, I64, ctypes.POINTER(AdamWParams), P, I, P], I),
         "hod_nccl_unique_id": ([P], I),
         "hod_nccl_comm_init": ([P, I, I, ctypes.POINTER(ctypes.c_void_p)], I),
         "hod_comm_destroy": ([P], I),
@@ -129,6 +128,7 @@ def load(build_if_missing: bool = True):
         "hod_all_gather_bf16": ([P, P, ctypes.c_size_t, P, P], I),
         "hod_all_reduce_f32": ([P, ctypes.c_size_t, P, P], I),
         "hod_p2p_step": ([ctypes.POINTER(P2PSpan), I, ctypes.POINTER(AdamWParams), P], I),
+        "hod_set_span_tma": ([I], I),
         "hod_p2p_barrier": ([P, I, I, I, ctypes.c_uint32, ctypes.c_uint32, ctypes.c_ulonglong, P, P], I),
         "hod_p2p_norm": ([P, I64, P, P, I, I, I, ctypes.c_uint32, ctypes.c_ulonglong, P, F, P, P, P, P], I),
         "hod_ce_copy": ([P, P, ctypes.c_size_t, P], I),

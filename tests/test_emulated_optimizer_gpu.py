@@ -24,10 +24,11 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def run_worker(*args, timeout=600):
+def run_worker(*args, timeout=600, extra_env=None):
     from paper_2312_03549_b200.emulation import child_env
 
     env = child_env()
+    env.update(extra_env or {})
     p = subprocess.run([sys.executable, str(ROOT / "tests" / "emu_worker.py"), *map(str, args)],
                        capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
     assert p.returncode == 0, f"worker failed ({p.returncode}):\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
@@ -39,6 +40,14 @@ def run_worker(*args, timeout=600):
 @pytest.mark.parametrize("flow", ["step", "hooks"])
 def test_emulated_ranks_match_oracle(d, clip, flow):
     out = run_worker("--d", d, "--clip", clip, "--flow", flow, "--steps", 3)
+    assert out["ok"] and out["buckets"] > 3
+
+
+@pytest.mark.parametrize("d,clip", [(2, 0.0), (4, 0.02), (8, 0.0)])
+def test_emulated_ranks_tma_span_kernel(d, clip):
+    """The TMA-fed span kernel (HOD_SPAN_TMA=2: also under the emulation's
+    grid cap) through the concurrent protocol, checked like the default."""
+    out = run_worker("--d", d, "--clip", clip, "--flow", "step", "--steps", 3, extra_env={"HOD_SPAN_TMA": "2"})
     assert out["ok"] and out["buckets"] > 3
 
 

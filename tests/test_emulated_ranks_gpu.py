@@ -1,4 +1,4 @@
-"""All DP degrees of the fused p2p kernel on ONE GPU, ranks emulated in turn.
+"""All DP degrees of the fused p2p kernels on ONE GPU, ranks emulated in turn.
 
 The box used for development has at most 4 GPUs, but the driver's scaling run
 uses 8.  Here every rank's buffers live on the same device: for rank r the
@@ -29,9 +29,18 @@ def u16(t):
     return t.detach().contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
 
 
+@pytest.fixture(params=["tma", "register"])
+def span_kernel(request, native):
+    """Both span kernels: the TMA-fed one (default for full-GPU launches) and
+    the register-streaming one (co-resident launches, NVLS)."""
+    nat.call("hod_set_span_tma", 1 if request.param == "tma" else 0)
+    yield request.param
+    nat.call("hod_set_span_tma", 1)
+
+
 @pytest.mark.parametrize("d", [2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("clip", [None, 0.02])
-def test_emulated_d_way_fused_step(oracle, native, d, clip):
+def test_emulated_d_way_fused_step(oracle, native, span_kernel, d, clip):
     gs = odd_tensors()
     L = build_bucket_layout(gs.numels, 200_000, dp=d)
     total, nb = L.total_numel, len(L.buckets)

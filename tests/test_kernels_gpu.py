@@ -284,24 +284,3 @@ def test_layout_of_gpt13b_stage_is_padding_free():
         gs = config_gradset("gpt13b", stage)
         L = build_bucket_layout(gs.numels, 25_000_000, dp=4)
         assert L.padding == 0
-
-
-@pytest.mark.parametrize("n,ctas", [(2048 * 37 + 1000, 0), (2048 * 300, 16), (5000, 3)])
-def test_tma_adamw_bit_exact(oracle, native, n, ctas):
-    """TMA-fed (cp.async.bulk + mbarrier ring) AdamW == oracle, incl. the tail path."""
-    gen = torch.Generator(device=DEV).manual_seed(n)
-    master = torch.randn(n, generator=gen, device=DEV).mul_(0.02)
-    m = torch.rand(n, generator=gen, device=DEV).mul_(1e-3)
-    v = torch.rand(n, generator=gen, device=DEV).mul_(1e-6)
-    g = torch.randn(n, generator=gen, device=DEV).mul_(1e-3).to(torch.bfloat16)
-    out = torch.empty(n, dtype=torch.bfloat16, device=DEV)
-    cm, cv, cp = master.cpu().numpy().copy(), m.cpu().numpy().copy(), v.cpu().numpy().copy()
-    for step in (1, 2, 3):
-        hp = nat.AdamWParams(1e-4, 0.9, 0.95, 1e-8, 0.1, step)
-        nat.call("hod_adamw_tma", master.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(), out.data_ptr(),
-                 n, ctypes.byref(hp), None, ctas, 0)
-        want = oracle.adamw(cm, cv, cp, u16(g), step)
-    torch.cuda.synchronize()
-    np.testing.assert_array_equal(u16(out), want)
-    np.testing.assert_array_equal(master.cpu().numpy().view(np.uint32), cm.view(np.uint32))
-    np.testing.assert_array_equal(v.cpu().numpy().view(np.uint32), cp.view(np.uint32))
