@@ -3,7 +3,7 @@
     ncu --set full --clock-control none --import-source on -k regex:'_kernel' \
         -o gpurun_out/prof_each python tools/ncu_each.py
 
-One GPU.  Kernels whose peers live on other GPUs (the fused span kernel in
+One GPU.  Kernels whose peers live on other GPUs (both span kernels in
 FUSED / RS / ADAMW_AG modes) run with all d ranks' buffers on this
 device and every barrier flag pre-set — the exact d-way code path with peer
 loads/stores turned into local ones (tools/fused_emulated.py) — so their DRAM
@@ -36,8 +36,11 @@ def entries(srcs):
     return e
 
 
-def span_kernel(d, mode, n_bucket=NB * 4):
-    """One emulated rank-0 launch of p2p_step_kernel over one bucket."""
+def span_kernel(d, mode, n_bucket=NB * 4, tma=1):
+    """One emulated rank-0 launch of a span kernel over one bucket (tma=1:
+    span_tma_kernel, the full-GPU default; 0: p2p_step_kernel, the
+    co-resident / NVLS one, here at full grid)."""
+    nat.call("hod_set_span_tma", tma)
     n = n_bucket // d
     grads = [torch.randn(n_bucket, device=DEV).mul_(1e-3).to(torch.bfloat16) for _ in range(d)]
     params = [torch.zeros(n_bucket, dtype=torch.bfloat16, device=DEV) for _ in range(d)]
@@ -66,7 +69,8 @@ def span_kernel(d, mode, n_bucket=NB * 4):
     assert int(err.item()) == 0
     # HBM bytes per owned element with the peers' copies local (see fused_emulated.py)
     per = {"fused": 2 * d + 24 + 2 * d, "rs": 2 * d + 2, "adamw_ag": 2 + 24 + 2 * d}[mode]
-    return {"name": f"span_{mode}_d{d}", "owned_elems": n, "algorithmic_bytes": per * n}
+    nat.call("hod_set_span_tma", 1)
+    return {"name": f"span_{'tma' if tma else 'reg'}_{mode}_d{d}", "owned_elems": n, "algorithmic_bytes": per * n}
 
 
 def main():
@@ -99,11 +103,12 @@ def main():
                                              ctypes.byref(HP), None, 0))
     k("pack_sumsq", 2 * NB, lambda: nat.call("hod_pack_sumsq", entries(half), 2, NB, ctypes.c_float(1.0), 0,
                                             parts.data_ptr(), 0))
-    for d in (2, 4, 8):
-        out.append(span_kernel(d, "fused"))
-    for mode in ("rs", "adamw_ag"):
-        for d in (2, 4):
-            out.append(span_kernel(d, mode))
+    for tma in (1, 0):
+        for d in (2, 4, 8):
+            out.append(span_kernel(d, "fused", tma=tma))
+        for mode in ("rs", "adamw_ag"):
+            for d in (2, 4, 8):
+                out.append(span_kernel(d, mode, tma=tma))
     print(json.dumps({"launch_order": out}))
 
 

@@ -22,7 +22,7 @@ from collections import defaultdict
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
-OURS = re.compile(r"hod::|pack_kernel|adamw_vec_kernel|adamw_scalar_kernel|sumsq_kernel|p2p_step_kernel|"
+OURS = re.compile(r"hod::|pack_kernel|adamw_vec_kernel|adamw_scalar_kernel|sumsq_kernel|p2p_step_kernel|span_tma_kernel|"
                   r"barrier_kernel|norm_exchange_kernel|sum_partials_kernel|clip_coef_kernel|pack_adamw|pack_sumsq|"
                   r"accumulate_partials")
 
@@ -103,9 +103,12 @@ def main():
     ap.add_argument("--note", default="")
     ap.add_argument("--each", help="path.ncu-rep of tools/ncu_each.py (one launch per kernel)")
     ap.add_argument("--each-order", help="tools/ncu_each.py stdout (launch order + algorithmic bytes)")
+    ap.add_argument("--out-dir", default=str(ROOT / "profiles"))
     a = ap.parse_args()
     if a.each:
-        order = json.loads(Path(a.each_order).read_text().strip().splitlines()[-1])["launch_order"]
+        line = next(x for x in reversed(Path(a.each_order).read_text().splitlines())
+                    if x.startswith('{"launch_order"'))   # ncu interleaves its ==PROF== lines
+        order = json.loads(line)["launch_order"]
         r = rep(Path(a.each), 1, 1, "none")["launches"]
         if len(r) != len(order):
             raise SystemExit(f"{len(r)} profiled launches vs {len(order)} in the launch order")
@@ -117,7 +120,7 @@ def main():
                       "traffic_over_algorithmic": round(tr / o["algorithmic_bytes"], 3),
                       "algorithmic_GBps": round(o["algorithmic_bytes"] / L["duration_us"] / 1e3, 1)})
             doc["kernels"][o["name"]] = L
-        out = ROOT / "profiles" / f"{a.round}_ncu_each.json"
+        out = Path(a.out_dir) / f"{a.round}_ncu_each.json"
         out.write_text(json.dumps(doc, indent=1) + "\n")
         print(out)
         return
@@ -143,7 +146,7 @@ def main():
         doc["kernels"][name] = {"source": Path(path).name, "launches": per_launch,
                                 "dram_bytes_per_launch": int(mean_traffic),
                                 "algorithmic_bytes_per_launch": int(mean_alg) if mean_alg else None}
-    out = ROOT / "profiles" / f"{a.round}_ncu_summary.json"
+    out = Path(a.out_dir) / f"{a.round}_ncu_summary.json"
     out.parent.mkdir(exist_ok=True)
     out.write_text(json.dumps(doc, indent=1) + "\n")
     print(out)
