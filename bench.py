@@ -202,14 +202,18 @@ def _emulated_traffic_ratio(dom: str, d: int, backend: str):
     local there.  p2p only (multicast has no single-GPU stand-in)."""
     if backend != "p2p":
         return None
+    # full-GPU p2p launches run the TMA-fed span kernel (round-2 captures name
+    # it span_tma_*); round-1 captures hold the register kernel as span_*
     for p in sorted((ROOT / "profiles").glob("*ncu_each.json"), reverse=True):
         try:
-            k = json.loads(p.read_text())["kernels"].get(f"span_{dom}_d{d}")
+            kernels = json.loads(p.read_text())["kernels"]
         except Exception:
             continue
-        if k and k.get("traffic_over_algorithmic"):
-            return {"traffic_over_algorithmic": k["traffic_over_algorithmic"], "source": f"{p.name}:span_{dom}_d{d}",
-                    "note": "one-GPU emulation of the d-way kernel (peer copies local), cold cache"}
+        for name in (f"span_tma_{dom}_d{d}", f"span_{dom}_d{d}"):
+            k = kernels.get(name)
+            if k and k.get("traffic_over_algorithmic"):
+                return {"traffic_over_algorithmic": k["traffic_over_algorithmic"], "source": f"{p.name}:{name}",
+                        "note": "one-GPU emulation of the d-way kernel (peer copies local), cold cache"}
     return None
 
 

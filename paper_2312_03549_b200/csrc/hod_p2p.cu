@@ -199,11 +199,18 @@ __device__ __forceinline__ void finish_item(const SpanArgs& a, const Item<D, kSr
           for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], f[k]);
         }
       }
+      uint16_t r[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) g[k] = bf16_to_f32(f32_to_bf16(acc[k]));
+      for (int k = 0; k < 4; ++k) {
+        r[k] = f32_to_bf16(acc[k]);
+        g[k] = bf16_to_f32(r[k]);
+      }
+      red[h] = make_uint2(r[0] | (static_cast<uint32_t>(r[1]) << 16), r[2] | (static_cast<uint32_t>(r[3]) << 16));
     }
     if (kMode != 2) {
-      if (kMode == 1 || a.keep_reduced) *reinterpret_cast<uint2*>(a.local_grad + it.e[h]) = pack4(g);
+      // red[h]: this quad's reduced bf16 bits (already rounded: no second pass)
+      if (kMode == 1 || a.keep_reduced) *reinterpret_cast<uint2*>(a.local_grad + it.e[h]) =
+          kSrc == kSrcNvls ? it.raw[h][0] : red[h];
       if (kMode == 1) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) ss = __fadd_rn(ss, __fmul_rn(g[k], g[k]));

@@ -205,10 +205,16 @@ __global__ void __launch_bounds__(kTmaBlock, 1) span_tma_kernel(const __grid_con
             for (int x = 0; x < 4; ++x) acc[x] = __fadd_rn(acc[x], f[x]);
           }
         }
+        uint16_t r[4];
 #pragma unroll
-        for (int x = 0; x < 4; ++x) g[x] = bf16_to_f32(f32_to_bf16(acc[x]));
+        for (int x = 0; x < 4; ++x) {
+          r[x] = f32_to_bf16(acc[x]);
+          g[x] = bf16_to_f32(r[x]);
+        }
         // the reduced quad replaces slot 0 (stored to the own shard)
-        if (kMode == 1 || a.keep_reduced) reinterpret_cast<uint2*>(st)[qd] = pack4(g);
+        if (kMode == 1 || a.keep_reduced)
+          reinterpret_cast<uint2*>(st)[qd] = make_uint2(r[0] | (static_cast<uint32_t>(r[1]) << 16),
+                                                        r[2] | (static_cast<uint32_t>(r[3]) << 16));
       }
       if constexpr (kMode == 1) {
 #pragma unroll

@@ -64,6 +64,16 @@ def test_emulated_ranks_fast_adamw_within_tolerance(d, clip):
     assert out["ok"]
 
 
+@pytest.mark.parametrize("adamw", ["exact", "fast"])
+def test_emulated_ranks_100_steps(adamw):
+    """The north star's long-run tolerance at d > 1: 100 steps of the real
+    protocol (d = 2, clip), every step against the oracle's INDEPENDENT
+    trajectory — exact: bit-exact at every step; fast: master / m / v within
+    1e-6 after step 1 and 1e-5 after that (norm-relative)."""
+    out = run_worker("--d", 2, "--clip", 0.02, "--steps", 100, "--adamw", adamw, timeout=1200)
+    assert out["ok"]
+
+
 def test_barrier_timeout_raises_device_error():
     out = run_worker("--d", 2, "--fault", "timeout", "--timeout", 0.5)
     assert "10003" in out["raised"] and "next_step_raised" in out
