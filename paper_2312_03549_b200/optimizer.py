@@ -158,7 +158,7 @@ class DistributedOptimizer:
                  sm_budget: int | None = None, span_numel: int = 256 * 2**20,
                  param_barriers: bool = True, pre_barrier: bool | None = None,
                  first_span_numel: int | None = None, symmetric=None, norm_symmetric=None,
-                 adamw: str = "exact"):
+                 adamw: str = "exact", corun_span_numel: int | None = None):
         if clip is not None and not clip > 0:
             raise InfeasibleConfigError(f"clip must be positive, got {clip}")
         init_params = list(init_params)
@@ -216,6 +216,13 @@ class DistributedOptimizer:
             first_span_numel = int(env)
         self.first_span_numel = (min(self.span_numel, 32 * 2**20) if first_span_numel is None
                                  else int(first_span_numel))
+        # co-resident spans (buckets delivered during backward) close early:
+        # a bucket that waits for its span to fill would otherwise run only
+        # after backward, at the end of the step, as exposed time
+        env = os.environ.get("HOD_CORUN_SPAN")
+        self.corun_span_numel = (int(env) if env is not None else
+                                 min(self.span_numel, 32 * 2**20) if corun_span_numel is None
+                                 else int(corun_span_numel))
         self._spans_launched = 0
         self._whole_step = False
         # p2p/nvls: a params-ready barrier after every span (enables per-bucket
@@ -883,7 +890,8 @@ class DistributedOptimizer:
                 self._queue_p2p(None, final=True)
             self._pending_span.append(bi)
         pend = self._pending_span
-        target = self.first_span_numel if self._spans_launched == 0 else self.span_numel
+        target = (self.first_span_numel if self._spans_launched == 0 else
+                  self.corun_span_numel if self._corun_active else self.span_numel)
         full = (sum(self.layout.buckets[x].numel for x in pend) >= target
                 or len(pend) == nat.HOD_P2P_MAX_SPAN)
         if pend and (full or final):
