@@ -36,8 +36,15 @@ from .symm import SymmetricTensor
 
 class PipelineRunner:
     def __init__(self, scenario, sr, opt, micro_batches: int | None = None, compute: bool = True,
-                 timeout_s: float = 30.0):
-        """``sr``: scenario_run.ScenarioRank of this rank; ``opt``: its optimizer."""
+                 timeout_s: float = 30.0, symmetric=None, stream=None):
+        """``sr``: scenario_run.ScenarioRank of this rank; ``opt``: its optimizer.
+
+        ``symmetric``: factory ``(numel, dtype, device, zero) ->`` symmetric
+        buffer over this rank's PP row (default: torch symmetric memory over a
+        PP-row process group, created collectively);
+        ``emulation.EmulatedRow(p).factory(stage - 1)`` runs the stages of a
+        row in one process on one GPU (the one-GPU test of the 1F1B
+        hand-offs).  ``stream``: the stream this rank's iteration runs on."""
         self.s, self.sr, self.opt = scenario, sr, opt
         self.device = opt.device
         m = scenario.model
@@ -53,15 +60,22 @@ class PipelineRunner:
         self.compute = compute
         self.timeout_ns = int(timeout_s * 1e9)
         self.epoch = 0
-        rows = [[r - 1 for r in row] for row in self._pp_rows()]
-        pg, _ = dist.new_subgroups_by_enumeration(rows)
+        emulated = symmetric is not None
+        if symmetric is None:
+            rows = [[r - 1 for r in row] for row in self._pp_rows()]
+            pg, _ = dist.new_subgroups_by_enumeration(rows)
+
+            def symmetric(numel, dtype, device, zero=False, _pg=pg):
+                return SymmetricTensor(numel, dtype, device, _pg, zero=zero)
         act = self.m * self.tokens * self.h
-        self.fwd_in = SymmetricTensor(act, torch.bfloat16, self.device, pg, zero=True)
-        self.bwd_in = SymmetricTensor(act, torch.bfloat16, self.device, pg, zero=True)
-        self.flags = SymmetricTensor(2 * self.m, torch.int32, self.device, pg, zero=True)
+        self.fwd_in = symmetric(act, torch.bfloat16, self.device, True)
+        self.bwd_in = symmetric(act, torch.bfloat16, self.device, True)
+        self.flags = symmetric(2 * self.m, torch.int32, self.device, True)
         self.err = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.trace: list = []     # compute=False: (op, micro, received tensor) for data-flow tests
-        self.stream = torch.cuda.current_stream(self.device)
+        self.op_events: list = []  # timed=True: (op, micro, start, end) CUDA events per stage op
+        self.timed = False
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         # stand-in layer weights: views of the optimizer's bf16 params, per layer
         self.layers = self._layer_weights()
         self.x = torch.randn(self.tokens, self.h, device=self.device, dtype=torch.bfloat16)
@@ -70,7 +84,8 @@ class PipelineRunner:
         self.gout = {w: torch.randn(self.tokens, w, device=self.device, dtype=torch.bfloat16) * 1e-3
                      for w in widths}
         torch.cuda.synchronize(self.device)
-        dist.barrier()
+        if not emulated:
+            dist.barrier()
 
     # ------------------------------------------------------------ plumbing
     def _pp_rows(self):
@@ -86,9 +101,14 @@ class PipelineRunner:
                 by_layer.setdefault(t.name.split(".")[1], []).append(i)
         return [by_layer[k] for k in sorted(by_layer, key=int)]
 
-    def _slot(self, sym: SymmetricTensor, q: int, k: int) -> torch.Tensor:
+    def _slot(self, sym, q: int, k: int) -> torch.Tensor:
+        """Micro-batch k's slot of rank q's receive buffer (a tensor view when
+        q is this rank; the peer's mapped address otherwise, used only as a
+        copy destination)."""
         n = self.tokens * self.h
-        return sym.handle.get_buffer(q, (self.m * n,), torch.bfloat16)[k * n:(k + 1) * n].view(self.tokens, self.h)
+        if q == self.pos:
+            return sym.tensor[k * n:(k + 1) * n].view(self.tokens, self.h)
+        return sym.peer(q, 2 * k * n)
 
     def _flag_ptr(self, q: int, kind: int, k: int) -> int:
         return self.flags.peer(q, 4 * (kind * self.m + k))
@@ -100,7 +120,7 @@ class PipelineRunner:
         # copy engine over NVLink (one peer: ~0.75 TB/s, tools/ce_probe.py); no
         # SM leaves the stage's GEMMs for the hand-off
         t = t.contiguous()
-        nat.call("hod_ce_copy", dst.data_ptr(), t.data_ptr(), t.numel() * t.element_size(),
+        nat.call("hod_ce_copy", dst, t.data_ptr(), t.numel() * t.element_size(),
                  nat.stream_ptr(self.stream))
         nat.call("hod_p2p_signal", self._flag_ptr(q, kind, k), self.epoch, nat.stream_ptr(self.stream))
 
@@ -158,6 +178,9 @@ class PipelineRunner:
                     self.opt.grad_ready(i, grads[i])
         for op, k in ops:
             idx = k - 1
+            if self.timed:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record(self.stream)
             if op == "fwd":
                 x = self.x if self.stage == 1 else self._recv(0, idx)
                 if not self.compute and self.stage > 1:
@@ -173,6 +196,10 @@ class PipelineRunner:
                 dx = self._backward(dy, last=(with_optimizer and k == self.m), grads=grads)
                 if self.stage > 1:
                     self._send(1, idx, dx)
+            if self.timed:
+                # the op's span on this stage's stream (receive wait included)
+                ev[1].record(self.stream)
+                self.op_events.append((op, k, ev[0], ev[1]))
         if with_optimizer:
             self.opt.finish_step()
 
