@@ -76,6 +76,7 @@ class PipelineRunner:
         self.op_events: list = []  # timed=True: (op, micro, start, end) CUDA events per stage op
         self.timed = False
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self.s_send = torch.cuda.Stream(device=self.device)
         # stand-in layer weights: views of the optimizer's bf16 params, per layer
         self.layers = self._layer_weights()
         self.x = torch.randn(self.tokens, self.h, device=self.device, dtype=torch.bfloat16)
@@ -117,12 +118,15 @@ class PipelineRunner:
         """kind 0: activation to the next stage; 1: gradient to the previous one."""
         q = self.pos + 1 if kind == 0 else self.pos - 1
         dst = self._slot(self.fwd_in if kind == 0 else self.bwd_in, q, k)
-        # copy engine over NVLink (one peer: ~0.75 TB/s, tools/ce_probe.py); no
-        # SM leaves the stage's GEMMs for the hand-off
+        # copy engine over NVLink (one peer: ~0.75 TB/s, tools/ce_probe.py) on a
+        # side stream: no SM leaves the stage's GEMMs for the hand-off, and the
+        # stage's next op does not queue behind the copy
         t = t.contiguous()
+        self.s_send.wait_stream(self.stream)
+        t.record_stream(self.s_send)
         nat.call("hod_ce_copy", dst, t.data_ptr(), t.numel() * t.element_size(),
-                 nat.stream_ptr(self.stream))
-        nat.call("hod_p2p_signal", self._flag_ptr(q, kind, k), self.epoch, nat.stream_ptr(self.stream))
+                 nat.stream_ptr(self.s_send))
+        nat.call("hod_p2p_signal", self._flag_ptr(q, kind, k), self.epoch, nat.stream_ptr(self.s_send))
 
     def _recv(self, kind: int, k: int) -> torch.Tensor:
         nat.call("hod_p2p_wait", self._flag_ptr(self.pos, kind, k), self.epoch, self.timeout_ns,
@@ -200,6 +204,9 @@ class PipelineRunner:
                 # the op's span on this stage's stream (receive wait included)
                 ev[1].record(self.stream)
                 self.op_events.append((op, k, ev[0], ev[1]))
+        # the next iteration reuses the neighbours' receive slots: its sends
+        # (and this iteration's end) are ordered after this iteration's sends
+        self.stream.wait_stream(self.s_send)
         if with_optimizer:
             self.opt.finish_step()
 
