@@ -20,7 +20,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libhod.so"
-SOURCES = ["hod_kernels.cu", "hod_nccl.cu", "hod_p2p.cu", "hod_span_tma.cu", "hod_ce.cu"]
+SOURCES = ["hod_kernels.cu", "hod_nccl.cu", "hod_p2p.cu", "hod_span_tma.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

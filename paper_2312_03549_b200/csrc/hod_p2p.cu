@@ -510,6 +510,20 @@ int hod_p2p_wait(const uint32_t* flag, uint32_t epoch, unsigned long long timeou
   return cuda_status(cudaGetLastError(), "hod_p2p_wait launch");
 }
 
+// Copy-engine transfer between a local and a peer-mapped (symmetric-memory)
+// address: the GPU's copy engines move the bytes over NVLink while every SM
+// stays with the GEMMs (pipeline stage hand-offs, the post-checkpoint
+// all-gather of restored param shards).  One peer at a time reaches
+// 718-755 GB/s per direction; three peers at once only 390-445 GB/s
+// (profiles/r01_ce_probe.jsonl), so the optimizer's own collectives stay on
+// SMs.
+int hod_ce_copy(void* dst, const void* src, size_t bytes, void* stream) {
+  if (bytes == 0) return HOD_OK;
+  if (!dst || !src) { set_error("hod_ce_copy: null pointer"); return HOD_EINVAL; }
+  return cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, static_cast<cudaStream_t>(stream)),
+                     "hod_ce_copy");
+}
+
 int hod_p2p_barrier(uint64_t* const* flags, int d, int rank, int slot, uint32_t epoch, uint32_t tag,
                     unsigned long long timeout_ns, uint32_t* err, void* stream) {
   if (!flags || d < 1 || d > kMaxRanks || rank < 0 || rank >= d || slot < 0) {
