@@ -35,7 +35,7 @@ from paper_2312_03549_b200.gradsets import config_gradset  # noqa: E402
 from paper_2312_03549_b200.synthetic import init_params  # noqa: E402
 
 
-def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: int = 0) -> dict:
+def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: int = 0, trace: str | None = None) -> dict:
     """Backward-only and full-iteration exposure of ``opt`` with a synthetic
     cuBLAS GEMM forward/backward of ``tokens`` tokens per GPU (see module doc)."""
     T = tokens
@@ -50,9 +50,14 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
     grads = [torch.empty(t.shape, device=dev, dtype=torch.bfloat16) for t in gs.tensors]
     order = [s.index for b in opt.layout.buckets for s in b.slots]   # backward order
 
-    def backward(feed_opt: bool):
+    bwd_events = []   # instrumented run: (tensor name, start, end) per backward op
+
+    def backward(feed_opt: bool, record: bool = False):
         for i in order:
             t = gs.tensors[i]
+            if record:
+                ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                ev[0].record()
             if len(t.shape) == 2:
                 out_f, in_f = t.shape
                 dy, x = acts[out_f], acts[in_f]
@@ -63,6 +68,9 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
                     torch.matmul(dy.t(), x, out=grads[i])                # dW = dY^T @ X
             else:
                 grads[i].normal_(0, 1e-3)
+            if record:
+                ev[1].record()
+                bwd_events.append((t.name, ev[0], ev[1]))
             if feed_opt:
                 opt.grad_ready(i, grads[i])
 
@@ -156,7 +164,7 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
     base.record()
     carve(True)
     opt.begin_step()
-    backward(True)
+    backward(True, record=trace is not None)
     end_bwd.record()
     opt.finish_step()
     carve(False)
@@ -165,6 +173,8 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
     opt._close_run()
     spans = [(name, base.elapsed_time(e0), base.elapsed_time(e1)) for name, e0, e1, *_ in opt._ktiming]
     opt.enable_kernel_timing(False)
+    if trace is not None:
+        write_trace(trace, base, bwd_events, spans, rank=dist.get_rank() if world > 1 else 0)
     busy_in_bwd = sum(max(0.0, min(e, bwd_end_ms) - s0) for _, s0, e in spans if s0 < bwd_end_ms)
     busy_total = sum(e - s0 for _, s0, e in spans)
     first_start = min((s0 for _, s0, _ in spans), default=0.0)
@@ -196,6 +206,24 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
     return doc
 
 
+def write_trace(path, base, bwd_events, spans, rank: int = 0) -> None:
+    """Chrome-trace JSON (chrome://tracing, Perfetto) of one instrumented
+    overlapped step: the backward ops on the compute stream and every
+    optimizer launch (pack, span / collective kernels) on its stream — the
+    overlap timeline the SURVEY's exposed-comm definition is read from
+    (CUDA events; nsys is not available in this image)."""
+    tid = {"pack": 1, "pack_sumsq": 1, "pack_adamw": 1}
+    ev = [{"name": name, "ph": "X", "pid": rank, "tid": 0, "ts": base.elapsed_time(e0) * 1e3,
+           "dur": e0.elapsed_time(e1) * 1e3, "cat": "backward"} for name, e0, e1 in bwd_events]
+    ev += [{"name": name, "ph": "X", "pid": rank, "tid": tid.get(name, 2), "ts": s0 * 1e3, "dur": (e - s0) * 1e3,
+            "cat": "optimizer"} for name, s0, e in spans]
+    meta = [{"name": "thread_name", "ph": "M", "pid": rank, "tid": k, "args": {"name": v}}
+            for k, v in ((0, "backward (compute stream)"), (1, "pack"), (2, "span / collective kernels"))]
+    p = path.replace("{rank}", str(rank))
+    with open(p, "w") as f:
+        json.dump({"traceEvents": meta + ev, "displayTimeUnit": "ms"}, f)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="gpt1.3b")
@@ -213,6 +241,7 @@ def main():
     ap.add_argument("--pre-barrier", type=int, default=None,
                     help="1: arrival barrier as a 1-CTA kernel before each span (optimizer pre_barrier)")
     ap.add_argument("--span-numel", type=int, default=None, help="fused-launch span threshold (elements)")
+    ap.add_argument("--trace", default=None, help="Chrome-trace JSON of one instrumented step ({rank} expands)")
     a = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -229,7 +258,7 @@ def main():
                                pre_barrier=None if a.pre_barrier is None else bool(a.pre_barrier),
                                **({"span_numel": a.span_numel} if a.span_numel else {}))
     del p0
-    doc = measure(opt, gs, a.tokens, a.iters, world, dev, gemm_carveout=a.gemm_carveout)
+    doc = measure(opt, gs, a.tokens, a.iters, world, dev, gemm_carveout=a.gemm_carveout, trace=a.trace)
     doc.update({"config": a.config, "bucket_size": a.bucket_size})
     if rank == 0:
         print(json.dumps(doc))
