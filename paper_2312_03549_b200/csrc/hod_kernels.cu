@@ -35,6 +35,15 @@ bool pdl_enabled() {
   return v;
 }
 
+// HOD_PACK_GENTLE=0: co-resident packs keep the full-GPU unroll (A/B runs)
+static bool pack_gentle() {
+  static const bool v = [] {
+    const char* e = getenv("HOD_PACK_GENTLE");
+    return !e || atoi(e) != 0;
+  }();
+  return v;
+}
+
 bool carveout_enabled() {
   static const bool v = [] {
     const char* e = getenv("HOD_CARVEOUT");
@@ -123,10 +132,15 @@ __device__ __forceinline__ void load8(const void* p, int64_t i, float (&f)[8]) {
   }
 }
 
-template <typename SrcT>
+// kUnroll: 16-byte vectors in flight per thread.  8 for full-GPU launches;
+// co-resident launches (beside GEMMs) take 2 — a quarter of the memory
+// pressure per SM, for a kernel that has the whole backward to finish.
+template <typename SrcT, int kUnroll = kPackUnroll>
 __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ PackTable t,
                                                          uint16_t* __restrict__ dst,
                                                          int64_t bucket_numel, float scale) {
+  constexpr int kPackTile = kThreads * kPackVec * kUnroll;
+  constexpr int kPackUnroll = kUnroll;
   pdl_trigger();  // the next bucket's pack touches disjoint memory
   const int64_t n_tiles = (bucket_numel + kPackTile - 1) / kPackTile;
   int e = 0;  // entry cursor; tiles visited by a CTA are increasing
@@ -541,10 +555,14 @@ int hod_pack_bf16(const hod_pack_entry* entries, int n_entries, uint16_t* bucket
     // measured best (unroll 8): 16 CTAs/SM cap for bf16 sources (6.2 TB/s), 3 for fp32 (6.6 TB/s)
     const int grid = grid_for((span + kPackTile - 1) / kPackTile, 1, src_dtype == HOD_DTYPE_BF16 ? 16 : 3);
     count_launch(1);
-    if (src_dtype == HOD_DTYPE_BF16)
-      launch_pdl(pack_kernel<uint16_t>, grid, kThreads, s, t, bucket + lo, span, scale);
-    else
-      launch_pdl(pack_kernel<float>, grid, kThreads, s, t, bucket + lo, span, scale);
+    const bool gentle = coresident() && pack_gentle();
+    if (src_dtype == HOD_DTYPE_BF16) {
+      if (gentle) launch_pdl(pack_kernel<uint16_t, 2>, grid, kThreads, s, t, bucket + lo, span, scale);
+      else launch_pdl(pack_kernel<uint16_t>, grid, kThreads, s, t, bucket + lo, span, scale);
+    } else {
+      if (gentle) launch_pdl(pack_kernel<float, 2>, grid, kThreads, s, t, bucket + lo, span, scale);
+      else launch_pdl(pack_kernel<float>, grid, kThreads, s, t, bucket + lo, span, scale);
+    }
     return cuda_status(cudaGetLastError(), "hod_pack_bf16 launch");
   });
 }
