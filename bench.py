@@ -195,6 +195,23 @@ def _traffic_from_profile(kernel: str):
     return None, None, None
 
 
+# best per-direction NVLink rate SM- or TMA-issued peer traffic reached on
+# this box for the span kernels' access mix (profiles/r02_peer_bw_tma_n2.jsonl,
+# r01_peer_bw_n4.jsonl, r01_nvls_bw_n4.jsonl); None where not measured
+_PRACTICAL_NVLINK = {
+    ("p2p", 2): (692.4, "d=2 TMA peer read + peer write (tma_both), r02_peer_bw_tma_n2.jsonl"),
+    ("p2p", 4): (659.9, "d=4 SM peer reads from 3 peers, r01_nvls_bw_n4.jsonl"),
+    ("nvls", 4): (580.0, "d=4 multimem.ld_reduce + multimem.st both ways, r01_nvls_bw_n4.jsonl"),
+}
+
+
+def _practical_nvlink(d: int, dom: str, backend: str):
+    v = _PRACTICAL_NVLINK.get((backend, d))
+    if v is None:
+        return None
+    return {"ceiling_gbps": v[0], "source": v[1]}
+
+
 def _emulated_traffic_ratio(dom: str, d: int, backend: str):
     """DRAM traffic / algorithmic bytes of the span kernel from the one-GPU
     emulated ncu capture (profiles/*_ncu_each.json, tools/ncu_each.py): a
@@ -746,6 +763,13 @@ def run_ours(args) -> None:
             phys = {"fused": 2 * (d_ + 1), "adamw_ag": 2 * d_, "rs": 2 * d_}[dom]
             nvl_view["physical_bytes_per_owned_element"] = phys
             nvl_view["physical_achieved"] = elems * phys / (ktime / 1e3) / 1e9 if ktime > 0 else None
+        # what SM/TMA-issued peer traffic reaches on this box (tools/peer_bw.py):
+        # the practical ceiling the span kernels are measured against
+        ceil = _practical_nvlink(d_, dom, opt.backend)
+        if ceil and nvl:
+            # NVLS ceilings are physical switch traffic: compare like with like
+            rate = nvl_view.get("physical_achieved") or nvl
+            nvl_view["practical"] = dict(ceil, achieved=rate, frac=rate / ceil["ceiling_gbps"])
         roof["traffic_emulated"] = _emulated_traffic_ratio(dom, d_, opt.backend)
         if hbm_elem / peak >= per_elem / NVLINK_PEAK:
             roof.update({"bound": "hbm", "achieved": hbm, "frac": hbm_view["frac"],
@@ -755,6 +779,7 @@ def run_ours(args) -> None:
                          "peak_source": "NVLink 5 nominal 900 GB/s per direction (north star, SURVEY §8d); "
                          "frac_measured_copy against the 770 GB/s peer copy of B200_PROFILING.md",
                          "frac_measured_copy": nvl_view["frac_measured_copy"], "hbm_view": hbm_view,
+                         "practical": nvl_view.get("practical"),
                          "nvlink_bytes_per_owned_element": per_elem, "bytes_per_element": per_elem})
             if "physical_achieved" in nvl_view:
                 roof["nvlink_physical"] = {k: nvl_view[k] for k in
