@@ -103,22 +103,43 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
         opt.finish_step(wait=False)   # the next forward waits bucket by bucket
         carve(False)
 
-    def timed(fn):
+    def params_ready():
+        """The current stream waits until every bucket's params are gathered
+        (an overlapped iteration's trailing update / all-gather counts)."""
+        for b in range(len(opt.layout.buckets)):
+            opt.wait_params(b)
+
+    def timed(fn, n=None, tail=None):
+        n = n or iters
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(iters):
+        for _ in range(n):
             fn()
+        if tail is not None:
+            tail()
         e1.record()
         torch.cuda.synchronize()
-        ms = e0.elapsed_time(e1) / iters
+        ms = e0.elapsed_time(e1) / n
         if world > 1:
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         return ms
+
+    def timed_pair(fa, fb, n=2, rounds=4):
+        """A and B alternated in blocks of ``n`` iterations (clock / power
+        drift hits both alike), median over ``rounds`` blocks each.  B's block
+        ends when its last update has gathered every bucket's params, so the
+        trailing optimizer work is charged once per block (steady state would
+        hide part of it behind the next forward: this errs high)."""
+        ra, rb = [], []
+        for _ in range(rounds):
+            ra.append(timed(fa, n))
+            rb.append(timed(fb, n, tail=params_ready))
+        return sorted(ra)[len(ra) // 2], sorted(rb)[len(rb) // 2]
 
     if gemm_carveout:
         # the SM carve-out is honoured by the cuBLASLt path
@@ -144,16 +165,14 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
         backward(False)
         opt.step(grads)
         overlapped()
-    t_bwd = timed(lambda: backward(False))
+    t_bwd, t_ovl = timed_pair(lambda: backward(False), overlapped)
     t_bwd_carved = timed(backward_carved) if gemm_carveout else t_bwd
     t_opt = timed(lambda: opt.step(grads))
-    t_ovl = timed(overlapped)
     for _ in range(2):
         iteration_ref()
         iteration_ovl()
     torch.cuda.synchronize()
-    t_it_ref = timed(iteration_ref)
-    t_it_ovl = timed(iteration_ovl)
+    t_it_ref, t_it_ovl = timed_pair(iteration_ref, iteration_ovl)
     # one instrumented overlapped step: where did the optimizer kernels run?
     base = torch.cuda.Event(enable_timing=True)
     end_bwd = torch.cuda.Event(enable_timing=True)
