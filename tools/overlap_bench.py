@@ -129,16 +129,19 @@ def measure(opt, gs, tokens: int, iters: int, world: int, dev, gemm_carveout: in
             ms = float(t.item())
         return ms
 
-    def timed_pair(fa, fb, n=2, rounds=4):
-        """A and B alternated in blocks of ``n`` iterations (clock / power
-        drift hits both alike), median over ``rounds`` blocks each.  B's block
-        ends when its last update has gathered every bucket's params, so the
-        trailing optimizer work is charged once per block (steady state would
-        hide part of it behind the next forward: this errs high)."""
+    def timed_pair(fa, fb, rounds=3):
+        """Steady-state per-iteration time of A and B: blocks of 1 and 3
+        iterations, each block timed until every bucket's params are gathered,
+        and the difference divided by 2 — the one trailing optimizer tail per
+        block cancels, so what is left is the iteration as it repeats (its
+        update overlapping the next forward).  A and B alternate block by
+        block (clock / power drift hits both alike); medians over rounds."""
         ra, rb = [], []
         for _ in range(rounds):
-            ra.append(timed(fa, n))
-            rb.append(timed(fb, n, tail=params_ready))
+            a1, b1 = timed(fa, 1, tail=params_ready), timed(fb, 1, tail=params_ready)
+            a3, b3 = timed(fa, 3, tail=params_ready), timed(fb, 3, tail=params_ready)
+            ra.append((a3 * 3 - a1) / 2)
+            rb.append((b3 * 3 - b1) / 2)
         return sorted(ra)[len(ra) // 2], sorted(rb)[len(rb) // 2]
 
     if gemm_carveout:
