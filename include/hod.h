@@ -34,7 +34,9 @@
 extern "C" {
 #endif
 
-#define HOD_ABI_VERSION 2
+/* 3: hod_adamw_tma removed (the TMA-fed path is the span kernel of
+ *    hod_p2p_step), hod_set_span_tma added */
+#define HOD_ABI_VERSION 3
 
 /* library-level error codes (outside the cudaError_t / ncclResult_t ranges) */
 #define HOD_OK 0

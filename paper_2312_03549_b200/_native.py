@@ -78,7 +78,7 @@ class AdamWParams(ctypes.Structure):
                 ("mode", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
-ABI_VERSION = 2          # HOD_ABI_VERSION of include/hod.h
+ABI_VERSION = 3          # HOD_ABI_VERSION of include/hod.h
 
 _lib = None
 _grid_base = 0

@@ -48,7 +48,7 @@ def test_python_binding_covers_header():
 
 def test_abi_version_and_error_slot(lib):
     lib.hod_abi_version.restype = ctypes.c_int
-    assert lib.hod_abi_version() == 2
+    assert lib.hod_abi_version() == 3
     lib.hod_last_error.restype = ctypes.c_char_p
     assert isinstance(lib.hod_last_error(), bytes)
 
