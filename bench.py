@@ -47,12 +47,17 @@ NVLINK_PEAK = NVLINK_NOMINAL   # headline roofline denominator; the measured cop
 KERNEL_NAMES = {
     "adamw": "hod adamw_vec_kernel (K2)",
     "pack": "hod pack_kernel (K1)",
-    "pack_push": "hod pack_push_kernel (K1 + RS transfer over NVLink)",
     "pack_adamw": "hod pack_adamw_kernel (K1+K2 fused, d=1)",
-    "fused": "hod p2p_step_kernel FUSED (barrier+RS+AdamW+AG)",
-    "rs": "hod p2p_step_kernel RS (+sumsq)",
-    "adamw_ag": "hod p2p_step_kernel ADAMW_AG",
+    "fused": "hod {span} FUSED (barrier+RS+AdamW+AG)",
+    "rs": "hod {span} RS (+sumsq)",
+    "adamw_ag": "hod {span} ADAMW_AG",
 }
+
+
+def _kernel_name(dom: str, backend: str) -> str:
+    """Full-GPU p2p span launches run the TMA-fed kernel, NVLS the register one."""
+    span = "span_tma_kernel" if backend == "p2p" else "p2p_step_kernel"
+    return KERNEL_NAMES.get(dom, dom).format(span=span)
 
 
 def _desc(cfg, clip) -> str:
@@ -731,7 +736,7 @@ def run_ours(args) -> None:
     n_launch, ktime, kbytes = kt.get(dom, (0, 0.0, 0))
     achieved = (kbytes / (ktime / 1e3)) / 1e9 if ktime > 0 else None
     traffic, alg_per_launch, prof = _traffic_from_profile(dom)
-    roof = {"kernel": KERNEL_NAMES.get(dom, dom), "bound": "hbm", "achieved": achieved, "peak": peak,
+    roof = {"kernel": _kernel_name(dom, opt.backend), "bound": "hbm", "achieved": achieved, "peak": peak,
             "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
             "traffic": traffic, "traffic_source": prof, "peak_source": peak_src,
             "traffic_launch_algorithmic_bytes": alg_per_launch,

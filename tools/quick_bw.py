@@ -49,10 +49,6 @@ print(f"sumsq n={n}: {t:.3f} ms  {2 * n / t / 1e6:.0f} GB/s")
 c = torch.empty_like(p)
 t = timeit(lambda: c.copy_(p))
 print(f"torch copy fp32 n={n}: {t:.3f} ms  {8 * n / t / 1e6:.0f} GB/s")
-for ctas in (0, 148, 74, 48, 32, 16):
-    t = timeit(lambda: nat.call("hod_adamw_tma", p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
-                                out.data_ptr(), n, ctypes.byref(hp), None, ctas, 0))
-    print(f"adamw_tma ctas={ctas or 'all'}: {t:.3f} ms  {28 * n / t / 1e6:.0f} GB/s")
 for lim in (148, 74, 48, 32, 16):
     nat.call("hod_set_grid_limit", lim * 4)
     t = timeit(lambda: nat.call("hod_adamw_bf16", p.data_ptr(), m.data_ptr(), v.data_ptr(), g.data_ptr(),
