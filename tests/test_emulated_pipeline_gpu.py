@@ -20,12 +20,18 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parent.parent
 
 
-def run(tmp_path, *args, timeout=900):
+def run(tmp_path, *args, timeout=900, data=2):
     from paper_2312_03549_b200.emulation import child_env
     from test_multigpu_gpu import MINI_PP_SCENARIO
 
+    doc = json.loads(json.dumps(MINI_PP_SCENARIO))
+    if data != 2:
+        # config 4's shape: PP = 2 x DP = d, one node of d GPUs per NIC cluster
+        doc["topology"]["gpus_per_node"] = data
+        doc["parallel"]["d"] = data
+        doc["model"]["global_batch"] = 4 * data
     scen = tmp_path / "mini_pp.json"
-    scen.write_text(json.dumps(MINI_PP_SCENARIO))
+    scen.write_text(json.dumps(doc))
     p = subprocess.run([sys.executable, str(ROOT / "tests" / "pipe_emu_worker.py"), "--scenario", str(scen),
                         *map(str, args)], capture_output=True, text=True, timeout=timeout, env=child_env(), cwd=ROOT)
     assert p.returncode == 0, f"worker failed ({p.returncode}):\n{p.stdout[-3000:]}\n{p.stderr[-3000:]}"
@@ -55,4 +61,18 @@ def test_pipeline_1f1b_handoffs_emulated(tmp_path):
         assert len(tr) == 2 * 4                  # 4 micro-batches x 2 iterations, one direction
         for op, k, mean, std in tr:
             # stage 1 sends x + 1 = 2; stage 2 returns (2 + 1) + 1 = 4
+            assert (op, mean, std) == (("fwd", 2.0, 0.0) if doc["stage"] == 2 else ("bwd", 4.0, 0.0))
+
+
+def test_pp2_dp4_scenario_emulated_matches_oracle(tmp_path):
+    """BASELINE config 4's exact shape (PP = 2 x DP = 4, eight ranks: DP rows
+    {0..3} / {4..7}, PP rows (q, q + 4), world clip norm over eight ranks) —
+    the layout the driver's 8-GPU run uses — with all eight ranks on one GPU."""
+    out = run(tmp_path, "--mode", "pipeline", "--clip", 0.05, "--steps", 2, "--micro", 4, data=4)
+    assert out["ok"]
+    assert out["stages"] == [1, 1, 1, 1, 2, 2, 2, 2]
+    assert out["dp_rows"] == [[0, 1, 2, 3], [4, 5, 6, 7]]
+    assert out["pp_rows"] == [[0, 4], [1, 5], [2, 6], [3, 7]]
+    for doc in out["traces"]:
+        for op, k, mean, std in doc["trace"]:
             assert (op, mean, std) == (("fwd", 2.0, 0.0) if doc["stage"] == 2 else ("bwd", 4.0, 0.0))
