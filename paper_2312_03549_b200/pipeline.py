@@ -184,9 +184,10 @@ class PipelineRunner:
             idx = k - 1
             if self.timed:
                 ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                ev[0].record(self.stream)
             if op == "fwd":
                 x = self.x if self.stage == 1 else self._recv(0, idx)
+                if self.timed:
+                    ev[0].record(self.stream)     # compute starts once the input is here
                 if not self.compute and self.stage > 1:
                     self.trace.append(("fwd", k, x.clone()))
                 y = self._forward(x)
@@ -195,13 +196,16 @@ class PipelineRunner:
                     self._send(0, idx, y)
             else:
                 dy = outs.pop(idx) if self.stage == self.p else self._recv(1, idx)
+                if self.timed:
+                    ev[0].record(self.stream)
                 if not self.compute and self.stage < self.p:
                     self.trace.append(("bwd", k, dy.clone()))
                 dx = self._backward(dy, last=(with_optimizer and k == self.m), grads=grads)
                 if self.stage > 1:
                     self._send(1, idx, dx)
             if self.timed:
-                # the op's span on this stage's stream (receive wait included)
+                # the op's compute on this stage's stream (from its input's
+                # arrival to its output's hand-off)
                 ev[1].record(self.stream)
                 self.op_events.append((op, k, ev[0], ev[1]))
         # the next iteration reuses the neighbours' receive slots: its sends

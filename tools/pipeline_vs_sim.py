@@ -55,6 +55,7 @@ def main():
     ap.add_argument("--scenario", required=True)
     ap.add_argument("--micro", type=int, default=8, help="micro-batches per iteration")
     ap.add_argument("--iters", type=int, default=2)
+    ap.add_argument("--timeline", default=None, help="write measured + simulated StageEvent timelines here")
     a = ap.parse_args()
     rank, local = int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -86,10 +87,26 @@ def main():
         ms = torch.tensor([e0.elapsed_time(e1) / a.iters], device=dev, dtype=torch.float64)
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
         iters[with_opt] = float(ms.item())
+    # one instrumented iteration: every stage op's span on its stream, against
+    # a common start (barrier + synchronize), in the reference's StageEvent
+    # form — the measured counterpart of SimReport.timeline (simulator.py:98-116)
+    pr.timed = True
+    pr.op_events = []
+    torch.cuda.synchronize()
+    dist.barrier()
+    base = torch.cuda.Event(enable_timing=True)
+    base.record(pr.stream)
+    pr.run_iteration(grads, with_optimizer=True)
+    torch.cuda.synchronize()
+    pr.timed = False
+    timeline = [{"stage": pr.stage, "rank": rank, "op": op, "micro": k,
+                 "start_s": base.elapsed_time(e0) / 1e3, "end_s": base.elapsed_time(e1) / 1e3}
+                for op, k, e0, e1 in pr.op_events]
     pr.check()
     opt.check_health()
     per = [None] * dist.get_world_size()
-    dist.all_gather_object(per, {"rank": rank, "stage": pr.stage, "t_f_ms": t_f, "t_b_ms": t_b})
+    dist.all_gather_object(per, {"rank": rank, "stage": pr.stage, "t_f_ms": t_f, "t_b_ms": t_b,
+                                 "timeline": timeline})
     if rank == 0:
         planned = hp.plan_scenario(s)
         part = hp.partition_scenario(s, topo=planned.topology)
@@ -135,6 +152,16 @@ def main():
                "note": "per-op times measured in isolation calibrate the reference cost model; the "
                        "simulator's PP hops are priced on the scenario's channels"}
         print(json.dumps(doc), flush=True)
+        if a.timeline:
+            # measured (DP-row rank 0 of each stage) and simulated timelines side by side
+            first = {}
+            for d in per:
+                first.setdefault(d["stage"], d)
+            sim_rep = simulator.simulate_iteration(topo, cfg, planned.plan, planned.channels, part, model, cost,
+                                                   exposed_dp_sync=exposed)
+            with open(a.timeline, "w") as f:
+                json.dump({"measured": [e for st in sorted(first) for e in first[st]["timeline"]],
+                           "simulated": [e.to_json_dict() for e in sim_rep.timeline]}, f)
     opt.close()
     dist.barrier()
     dist.destroy_process_group()
