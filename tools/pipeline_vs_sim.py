@@ -7,7 +7,8 @@ Runs ``pipeline.PipelineRunner`` (the 1F1B order of simulator._one_f_one_b,
 stage hand-offs over NVLink peer memory, cuBLAS GEMM stand-ins on the
 stage's real parameters, the DP optimizer overlapping the last micro-batch's
 backward) and measures, per stage, the forward and backward time of one
-micro-batch in isolation (CUDA events, no hand-off waits).  Those per-op
+micro-batch in isolation at sustained clocks (CUDA events, no hand-off
+waits, after ~1 s of back-to-back warm-up).  Those per-op
 times calibrate the reference's cost model — ``CostModel(cluster_speeds_tflops=…,
 backward_forward_ratio=…)`` so that ``stage_compute_time`` reproduces them —
 and ``simulate_iteration`` (the event-driven 1F1B of simulator.py:359-470)
@@ -38,8 +39,20 @@ from paper_2312_03549_b200.scenario_run import make_optimizer, setup_rank  # noq
 from paper_2312_03549_b200.synthetic import init_params, make_grads  # noqa: E402
 
 
-def _time(fn, reps, stream):
+def _time(fn, reps, stream, warm_s: float = 1.0):
+    """Mean time of ``fn`` at SUSTAINED clocks: ~``warm_s`` of back-to-back
+    warm-up first (a B200 running GEMMs at full power settles well below its
+    burst clock — MEASURED_PEAKS.json: sustained bf16 0.85 of burst), then
+    ``reps`` timed calls."""
     fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    for _ in range(max(1, int(warm_s * 1e3 / max(e0.elapsed_time(e1), 1e-3)))):
+        fn()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -69,8 +82,8 @@ def main():
 
     # per-op compute of this stage in isolation
     dy = torch.randn(pr.tokens, pr.h, device=dev, dtype=torch.bfloat16) * 1e-3
-    t_f = _time(lambda: pr._forward(pr.x), 5, pr.stream)
-    t_b = _time(lambda: pr._backward(dy, last=False, grads=grads), 5, pr.stream)
+    t_f = _time(lambda: pr._forward(pr.x), 20, pr.stream)
+    t_b = _time(lambda: pr._backward(dy, last=False, grads=grads), 20, pr.stream)
 
     iters = {}
     for with_opt in (False, True):
@@ -149,8 +162,8 @@ def main():
                "simulated_iter_ms_measured_exposed_dp": sim(exposed_dp_sync=exposed),
                "measured_exposed_dp_ms": exposed * 1e3,
                "ideal_1f1b_ms": (a.micro + cfg.pipeline - 1) * max(tf[st] + tb[st] for st in tf),
-               "note": "per-op times measured in isolation calibrate the reference cost model; the "
-                       "simulator's PP hops are priced on the scenario's channels"}
+               "note": "per-op times measured in isolation at sustained clocks calibrate the reference cost "
+                       "model; the simulator's PP hops are priced on the scenario's channels"}
         print(json.dumps(doc), flush=True)
         if a.timeline:
             # measured (DP-row rank 0 of each stage) and simulated timelines side by side
