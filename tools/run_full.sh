@@ -21,7 +21,7 @@ if [ $N -ge 4 ]; then
   TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1"
   timeout 900 $TR --master-port 29704 bench.py --gpus 4 --steps 5 --scenario scenarios/gpt13b_pp2_dp2_hybrid.json \
     > $O/${TAG}_bench_gpt13b_pp2dp2_n4.log 2>&1
-  timeout 900 $TR --master-port 29714 tools/pipeline_vs_sim.py --scenario scenarios/gpt13b_pp2_dp2_hybrid.json --micro 8 \
+  timeout 900 $TR --master-port 29714 tools/pipeline_vs_sim.py --scenario scenarios/gpt13b_pp2_dp2_hybrid.json --micro 8 --timeline $O/${TAG}_pipeline_timeline_gpt13b_n4.json \
     > $O/${TAG}_pipeline_vs_sim_gpt13b_n4.log 2>&1
 fi
 timeout 600 python bench.py --impl reference > $O/${TAG}_bench_reference_n1.log 2>&1
