@@ -48,7 +48,6 @@ def u16(t):
 
 def check(opts, grads, state, coefs, norms, step, clip):
     """Every stage's DP row against the oracle (independent trajectory)."""
-    world = len(opts)
     rows = sorted({o.group.ranks for o in opts})
     reduced = {}
     for row in rows:
@@ -86,7 +85,6 @@ def check(opts, grads, state, coefs, norms, step, clip):
                 for name, dv, ov in zip(("master", "m", "v"), dev_state, (master, m, v)):
                     assert np.array_equal(dv[offs[bi]:offs[bi] + n].view(np.uint32), ov.view(np.uint32)), \
                         f"step {step} rank {q} bucket {bi}: {name}"
-    del world
 
 
 def main():
