@@ -1,7 +1,7 @@
-"""BASELINE config 4 in miniature (PP = 2 x DP = 2) with every rank on ONE GPU.
+"""BASELINE config 4 in miniature (PP = 2 x DP = 2 or 4) with every rank on ONE GPU.
 
 Launched by tests/test_emulated_pipeline_gpu.py in a fresh process
-(emulation.child_env).  The reference-compatible plan places the four ranks
+(emulation.child_env).  The reference-compatible plan places the ranks
 (stage, DP row, PP row: planner.optimizer_placement over groups.py Eq. 2/3);
 each DP row, each PP row and the world-wide clip-norm group become an
 ``emulation.EmulatedRow``, so the ranks run the real protocol concurrently on
