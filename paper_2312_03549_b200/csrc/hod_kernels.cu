@@ -379,13 +379,16 @@ __global__ void __launch_bounds__(kSumsqThreads) sumsq_kernel(const uint16_t* __
 // clipping needs the norm before the fused pack+AdamW, and this pass costs
 // 2 B/element instead of the 4 + 2 of pack-then-sumsq.  Fixed grid, fixed
 // per-thread order => reproducible partials.
-template <typename SrcT>
-__global__ void __launch_bounds__(kSumsqThreads) pack_sumsq_kernel(const __grid_constant__ PackTable t,
-                                                                    int64_t numel, float scale,
-                                                                    float* __restrict__ partials,
-                                                                    int accumulate) {
-  constexpr int kThreads = kSumsqThreads;
-  constexpr int kPackTile = kSumsqTile;
+// kT threads per CTA: 1024 for full-GPU launches; 256 for co-resident ones
+// (a 1024-thread CTA needs 31.7 K registers, more than the 22.5 K a GEMM CTA
+// leaves on its SM).
+template <typename SrcT, int kT = kSumsqThreads>
+__global__ void __launch_bounds__(kT) pack_sumsq_kernel(const __grid_constant__ PackTable t,
+                                                         int64_t numel, float scale,
+                                                         float* __restrict__ partials,
+                                                         int accumulate) {
+  constexpr int kThreads = kT;
+  constexpr int kPackTile = kT * kPackVec * kSumsqUnroll;
   pdl_trigger();  // the next bucket's norm pass writes other partial slots
   // 8 independent accumulators (one per vector lane), folded in a fixed order
   // at the end: breaks the serial FADD chain, stays reproducible
@@ -431,7 +434,7 @@ __global__ void __launch_bounds__(kSumsqThreads) pack_sumsq_kernel(const __grid_
   float acc = 0.0f;
 #pragma unroll
   for (int k = 0; k < 8; ++k) acc = __fadd_rn(acc, acc8[k]);
-  const float sblk = block_sum<kSumsqThreads>(acc);
+  const float sblk = block_sum<kT>(acc);
   // windows after the first of a > HOD_PACK_MAX_ENTRIES table add onto the
   // partials of the windows before them (fixed window order: reproducible)
   if (threadIdx.x == 0) partials[blockIdx.x] = accumulate ? __fadd_rn(partials[blockIdx.x], sblk) : sblk;
@@ -622,7 +625,15 @@ int hod_pack_sumsq(const hod_pack_entry* entries, int n_entries, int64_t bucket_
     // at entry: the next bucket's norm pass writes other partial slots.
     const int acc = window++ > 0;
     const int grid = partials_grid();
-    if (!acc) {
+    if (coresident()) {
+      if (src_dtype == HOD_DTYPE_BF16) {
+        if (!acc) launch_pdl(pack_sumsq_kernel<uint16_t, 256>, grid, 256, s, t, span, scale, partials, 0);
+        else launch(pack_sumsq_kernel<uint16_t, 256>, grid, 256, 0, s, t, span, scale, partials, 1);
+      } else {
+        if (!acc) launch_pdl(pack_sumsq_kernel<float, 256>, grid, 256, s, t, span, scale, partials, 0);
+        else launch(pack_sumsq_kernel<float, 256>, grid, 256, 0, s, t, span, scale, partials, 1);
+      }
+    } else if (!acc) {
       if (src_dtype == HOD_DTYPE_BF16)
         launch_pdl(pack_sumsq_kernel<uint16_t>, grid, kSumsqThreads, s, t, span, scale, partials, 0);
       else

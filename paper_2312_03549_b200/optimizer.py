@@ -984,8 +984,12 @@ class DistributedOptimizer:
         # into one launch measured slower: 6.37 vs 6.55 TB/s on LLaMA-7B — a
         # grid striding over a ~37 GB range loses DRAM locality.)
         coef = _ptr(self._coef)
-        for bi, entries, dtype in sorted(self._deferred_pa, key=lambda t: t[0], reverse=True):
-            self._pack_adamw(bi, entries, dtype, coef, chained=True)
+        # with finish_step(wait=False) the next forward runs concurrently: the
+        # first update gets the whole GPU (the forward waits for it), the rest
+        # run co-resident beside the forward GEMMs (as the p2p post-norm spans)
+        for k, (bi, entries, dtype) in enumerate(sorted(self._deferred_pa, key=lambda t: t[0], reverse=True)):
+            with self._coresident(k > 0 and not self._finish_wait and not self._whole_step):
+                self._pack_adamw(bi, entries, dtype, coef, chained=True)
         self._deferred_pa = []
 
     def _clip_and_update(self) -> None:
