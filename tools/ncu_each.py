@@ -109,6 +109,22 @@ def main():
         for mode in ("rs", "adamw_ag"):
             for d in (2, 4, 8):
                 out.append(span_kernel(d, mode, tma=tma))
+    # the CO-RESIDENT variants that run beside the backward GEMMs (grid cap 148:
+    # one CTA per SM, register span kernel with one item per thread, the
+    # unroll-2 pack, max shared-memory carveout) — measured here alone
+    nat.set_grid_base(148)
+    try:
+        k("pack_bf16_coresident", 4 * NB, lambda: nat.call("hod_pack_bf16", entries(half), 2, bucket.data_ptr(), NB,
+                                                           ctypes.c_float(0.5), 0, 0))
+        for d in (2, 4):
+            doc = span_kernel(d, "fused", tma=1)
+            doc["name"] = f"span_coresident_fused_d{d}"
+            out.append(doc)
+        doc = span_kernel(2, "rs", tma=1)
+        doc["name"] = "span_coresident_rs_d2"
+        out.append(doc)
+    finally:
+        nat.set_grid_base(0)
     print(json.dumps({"launch_order": out}))
 
 
