@@ -550,7 +550,8 @@ def north_star_probe(args, world: int, rank: int, dev) -> dict:
                        "t_fwd_bwd_ms": o["iteration"]["t_fwd_bwd_ms"],
                        "t_fwd_bwd_opt_ms": o["iteration"]["t_fwd_bwd_opt_ms"],
                        "exposed_comm_frac_survey": o["exposed_comm_frac_survey"],
-                       "t_optimizer_alone_ms": o["t_optimizer_alone_ms"]}}
+                       "t_optimizer_alone_ms": o["t_optimizer_alone_ms"],
+                       "hidden_frac_of_optimizer": o["hidden_frac_of_optimizer"]}}
     opt.close()
     torch.cuda.empty_cache()
     return out
@@ -867,8 +868,11 @@ def run_ours(args) -> None:
                    "exposed_comm_frac_survey": o["exposed_comm_frac_survey"],
                    "t_backward_ms": o["t_backward_ms"], "t_backward_with_opt_ms": o["t_overlapped_ms"],
                    "t_optimizer_alone_ms": o["t_optimizer_alone_ms"],
+                   "hidden_frac_of_optimizer": o["hidden_frac_of_optimizer"],
                    "note": "synthetic GEMM fwd/bwd (real cuBLAS bf16 GEMMs on the config's weight shapes); "
-                           "exposed_frac_iteration = (iter with optimizer - iter without) / iter with"}
+                           "exposed_frac_iteration = (iter with optimizer - iter without) / iter with, "
+                           "steady state: (T(3 iterations) - T(1)) / 2 per block, blocks alternated with / "
+                           "without, medians (tools/overlap_bench.py)"}
 
     opt_info = {"buckets": len(opt.layout.buckets), "dp": opt.dp, "backend": opt.backend}
     # ---- self-check after every timed measurement (one more step vs the oracle)
