@@ -333,7 +333,6 @@ static int launch_adamw(float* master, float* exp_avg, float* exp_avg_sq, const 
 // read-only streams use 1024-thread CTAs to fill the SM (2048 threads).
 constexpr int kSumsqThreads = 1024;
 constexpr int kSumsqUnroll = 2;
-constexpr int kSumsqTile = kSumsqThreads * kPackVec * kSumsqUnroll;   // 16384 elements
 
 template <int NT>
 __device__ __forceinline__ float block_sum(float x) {
