@@ -63,6 +63,31 @@ def _time(fn, reps, stream, warm_s: float = 1.0):
     return e0.elapsed_time(e1) / reps
 
 
+def calibrated_model(s, micro: int, tf: dict, tb: dict):
+    """The reference's cost model calibrated to measured per-op times:
+    ``tf`` / ``tb`` map stage -> forward / backward ms of one micro-batch.
+    Returns (planned, partition, model, CostModel) such that
+    ``stage_compute_time`` reproduces ``tf`` on every stage (each stage's
+    cluster speed solved for) with ``backward_forward_ratio`` = sum(tb) /
+    sum(tf); the model's global batch is rescaled so the simulator schedules
+    ``micro`` micro-batches."""
+    from dataclasses import replace
+
+    planned = hp.plan_scenario(s)
+    part = hp.partition_scenario(s, topo=planned.topology)
+    cfg, topo, model = planned.config, planned.topology, s.model
+    if simulator.micro_batch_count(model, cfg) != micro:
+        model = replace(model, global_batch=micro * model.micro_batch * cfg.data)
+    ratio = sum(tb.values()) / sum(tf.values())
+    speeds = [None] * len(topo.clusters)
+    for st in range(1, cfg.pipeline + 1):
+        f_at_1tf, _ = simulator.stage_compute_time(part.stage_layers[st - 1], model, cfg, 1.0, 1.0, ratio)
+        speeds[simulator._stage_cluster(st, cfg, topo) - 1] = f_at_1tf / (tf[st] / 1e3)
+    speeds = [x if x is not None else max(v for v in speeds if v) for x in speeds]
+    cost = simulator.CostModel(backward_forward_ratio=ratio, cluster_speeds_tflops=tuple(speeds))
+    return planned, part, model, cost
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scenario", required=True)
@@ -121,15 +146,6 @@ def main():
     dist.all_gather_object(per, {"rank": rank, "stage": pr.stage, "t_f_ms": t_f, "t_b_ms": t_b,
                                  "timeline": timeline})
     if rank == 0:
-        planned = hp.plan_scenario(s)
-        part = hp.partition_scenario(s, topo=planned.topology)
-        cfg, topo, model = planned.config, planned.topology, s.model
-        # the simulator's micro-batch count is the scenario's; ours is --micro:
-        # rescale the global batch so both schedules run the same m
-        m_sim = simulator.micro_batch_count(model, cfg)
-        if m_sim != a.micro:
-            from dataclasses import replace
-            model = replace(model, global_batch=a.micro * model.micro_batch * cfg.data)
         stage_tf = {}
         stage_tb = {}
         for d in per:
@@ -137,15 +153,9 @@ def main():
             stage_tb.setdefault(d["stage"], []).append(d["t_b_ms"])
         tf = {st: sum(v) / len(v) for st, v in stage_tf.items()}
         tb = {st: sum(v) / len(v) for st, v in stage_tb.items()}
-        ratio = sum(tb.values()) / sum(tf.values())
-        # calibrate: stage_compute_time(..., eta = 1, device_tflops_peak = speed) == measured t_f
-        speeds = [None] * len(topo.clusters)
-        for st in range(1, cfg.pipeline + 1):
-            f_at_1tf, _ = simulator.stage_compute_time(part.stage_layers[st - 1], model, cfg, 1.0, 1.0, ratio)
-            c = simulator._stage_cluster(st, cfg, topo)
-            speeds[c - 1] = f_at_1tf / (tf[st] / 1e3)
-        speeds = [x if x is not None else max(v for v in speeds if v) for x in speeds]
-        cost = simulator.CostModel(backward_forward_ratio=ratio, cluster_speeds_tflops=tuple(speeds))
+        planned, part, model, cost = calibrated_model(s, a.micro, tf, tb)
+        cfg, topo = planned.config, planned.topology
+        speeds, ratio = list(cost.cluster_speeds_tflops), cost.backward_forward_ratio
         sim = lambda **kw: simulator.simulate_iteration(topo, cfg, planned.plan, planned.channels, part,  # noqa: E731
                                                         model, cost, **kw).iter_time_s * 1e3
         sim_no_dp = sim(exposed_dp_sync=0.0)
