@@ -51,6 +51,15 @@ def test_emulated_ranks_tma_span_kernel(d, clip):
     assert out["ok"] and out["buckets"] > 3
 
 
+@pytest.mark.parametrize("flow", ["step", "hooks"])
+def test_emulated_baseline_config1_toy_gpt_fp32_dp2(flow):
+    """BASELINE config 1 exactly (toy GPT L4 h256, fp32 grads, DP = 2, one
+    overlapped step) — the reference's CPU scenario — on one GPU."""
+    out = run_worker("--d", 2, "--config", "toy", "--grad-dtype", "f32", "--bucket", 4_000_000,
+                     "--span", 8_000_000, "--first-span", 4_000_000, "--flow", flow, "--steps", 2)
+    assert out["ok"]
+
+
 def test_emulated_fp32_grads_without_keep_reduced():
     out = run_worker("--d", 4, "--grad-dtype", "f32", "--keep-reduced", 0, "--clip", 1.0, "--flow", "hooks")
     assert out["ok"]
