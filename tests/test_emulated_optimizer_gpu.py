@@ -60,6 +60,17 @@ def test_emulated_baseline_config1_toy_gpt_fp32_dp2(flow):
     assert out["ok"]
 
 
+@pytest.mark.parametrize("d,clip", [(2, 0.0), (4, 1.0)])
+def test_emulated_fullsize_gpt13b(d, clip):
+    """BASELINE config 2 at its real size (GPT-3 1.3B gradient set, 37
+    buckets of 25 M elements, bf16 grads) with d ranks running the real
+    protocol on one GPU: every bucket of every rank bit-exact against the
+    oracle (reduced shard, master, m, v, gathered params)."""
+    out = run_worker("--d", d, "--config", "gpt1.3b", "--bucket", 25_000_000, "--span", 268_435_456,
+                     "--first-span", 33_554_432, "--clip", clip, "--steps", 1, "--timeout", 60, timeout=1200)
+    assert out["ok"] and out["buckets"] == 37
+
+
 def test_emulated_fp32_grads_without_keep_reduced():
     out = run_worker("--d", 4, "--grad-dtype", "f32", "--keep-reduced", 0, "--clip", 1.0, "--flow", "hooks")
     assert out["ok"]
