@@ -33,9 +33,10 @@ overlapped operation.  The ``backend`` selects how C1/C2 move bytes:
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
-import os
 import math
+import os
 from dataclasses import dataclass, field
 
 import torch
@@ -671,7 +672,6 @@ class DistributedOptimizer:
     def _coresident(self, on: bool):
         """Context: launches inside it use the co-resident grid (sm_budget)
         when ``on`` — they share the SMs with the caller's GEMMs."""
-        import contextlib
 
         @contextlib.contextmanager
         def ctx():
