@@ -631,7 +631,6 @@ class DistributedOptimizer:
     def no_sync(self):
         """Context manager: hooks registered by ``register_hooks`` do not
         deliver gradients inside it (gradient-accumulation micro-batches)."""
-        import contextlib
 
         @contextlib.contextmanager
         def ctx():
