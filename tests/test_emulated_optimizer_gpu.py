@@ -43,6 +43,15 @@ def test_emulated_ranks_match_oracle(d, clip, flow):
     assert out["ok"] and out["buckets"] > 3
 
 
+@pytest.mark.parametrize("d", [5, 6, 7])
+def test_emulated_ranks_non_power_of_two(d):
+    """DP rows that are not a power of two (the generic-d kernel paths, shard
+    padding to lcm(128, 16 d)) through the concurrent protocol with clipping
+    and the hook-driven flow."""
+    out = run_worker("--d", d, "--clip", 0.02, "--flow", "hooks", "--steps", 2)
+    assert out["ok"]
+
+
 @pytest.mark.parametrize("d,clip", [(2, 0.0), (4, 0.02), (8, 0.0)])
 def test_emulated_ranks_tma_span_kernel(d, clip):
     """The TMA-fed span kernel (HOD_SPAN_TMA=2: also under the emulation's
