@@ -121,4 +121,7 @@ def config_gradset(config: str, stage: int = 1) -> GradSet:
                                  first_layer=first, name=f"gpt3-13b-stage{stage}")
     if config == "odd":
         return odd_tensors()
+    if config == "deep":
+        # many small tensors: > HOD_P2P_MAX_SPAN buckets at small bucket sizes (test shape)
+        return gpt_stage_tensors(40, 128, 1000, name="deep-gpt-l40-h128")
     raise ValueError(f"unknown gradient-set config {config!r}")

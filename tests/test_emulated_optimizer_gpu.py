@@ -43,6 +43,17 @@ def test_emulated_ranks_match_oracle(d, clip, flow):
     assert out["ok"] and out["buckets"] > 3
 
 
+@pytest.mark.parametrize("flow", ["step", "hooks"])
+def test_emulated_ranks_maximum_span(flow):
+    """Spans at their maximum of HOD_P2P_MAX_SPAN (32) buckets: a deep model
+    of many small tensors, one bucket each, with an unbounded span threshold
+    splits into full 32-bucket spans and a remainder (one launch's SpanArgs
+    tables filled to capacity)."""
+    out = run_worker("--d", 2, "--config", "deep", "--bucket", 20_000, "--span", 10**9, "--first-span", 10**9,
+                     "--clip", 0.02, "--flow", flow, "--steps", 2)
+    assert out["ok"] and out["buckets"] > 32
+
+
 @pytest.mark.parametrize("d", [5, 6, 7])
 def test_emulated_ranks_non_power_of_two(d):
     """DP rows that are not a power of two (the generic-d kernel paths, shard
