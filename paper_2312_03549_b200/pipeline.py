@@ -102,14 +102,15 @@ class PipelineRunner:
                 by_layer.setdefault(t.name.split(".")[1], []).append(i)
         return [by_layer[k] for k in sorted(by_layer, key=int)]
 
-    def _slot(self, sym, q: int, k: int) -> torch.Tensor:
-        """Micro-batch k's slot of rank q's receive buffer (a tensor view when
-        q is this rank; the peer's mapped address otherwise, used only as a
-        copy destination)."""
+    def _own_slot(self, sym, k: int) -> torch.Tensor:
+        """Micro-batch k's slot of this rank's receive buffer."""
         n = self.tokens * self.h
-        if q == self.pos:
-            return sym.tensor[k * n:(k + 1) * n].view(self.tokens, self.h)
-        return sym.peer(q, 2 * k * n)
+        return sym.tensor[k * n:(k + 1) * n].view(self.tokens, self.h)
+
+    def _peer_slot_ptr(self, sym, q: int, k: int) -> int:
+        """Device address of micro-batch k's slot in rank q's receive buffer
+        (peer-mapped; a copy destination)."""
+        return sym.peer(q, 2 * k * self.tokens * self.h)
 
     def _flag_ptr(self, q: int, kind: int, k: int) -> int:
         return self.flags.peer(q, 4 * (kind * self.m + k))
@@ -117,7 +118,7 @@ class PipelineRunner:
     def _send(self, kind: int, k: int, t: torch.Tensor) -> None:
         """kind 0: activation to the next stage; 1: gradient to the previous one."""
         q = self.pos + 1 if kind == 0 else self.pos - 1
-        dst = self._slot(self.fwd_in if kind == 0 else self.bwd_in, q, k)
+        dst = self._peer_slot_ptr(self.fwd_in if kind == 0 else self.bwd_in, q, k)
         # copy engine over NVLink (one peer: ~0.75 TB/s, tools/ce_probe.py) on a
         # side stream: no SM leaves the stage's GEMMs for the hand-off, and the
         # stage's next op does not queue behind the copy
@@ -131,7 +132,7 @@ class PipelineRunner:
     def _recv(self, kind: int, k: int) -> torch.Tensor:
         nat.call("hod_p2p_wait", self._flag_ptr(self.pos, kind, k), self.epoch, self.timeout_ns,
                  self.err.data_ptr(), nat.stream_ptr(self.stream))
-        return self._slot(self.fwd_in if kind == 0 else self.bwd_in, self.pos, k)
+        return self._own_slot(self.fwd_in if kind == 0 else self.bwd_in, k)
 
     # ------------------------------------------------------------ compute
     def _forward(self, x: torch.Tensor) -> torch.Tensor:
