@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--kernel", default="adamw", choices=["adamw", "fused_d2", "pack"])
     ap.add_argument("--grids", default="0,148,296,592")
+    ap.add_argument("--green", type=int, default=0,
+                    help="run the optimizer kernel on a CUDA green context of this many SMs (the GEMMs keep "
+                         "the primary context)")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     h, T = a.hidden, a.tokens
@@ -87,6 +90,10 @@ def main():
         _native.check(rc, a.kernel)
 
     sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    if a.green:
+        gctx = torch.cuda.green_contexts.GreenContext.create(a.green, 0)
+        gs_ = gctx.Stream()
+        sb = torch.cuda.Stream(stream_id=gs_.stream_id, device_index=gs_.device_index, device_type=gs_.device_type)
 
     def timed(fn):
         best = None
@@ -125,6 +132,7 @@ def main():
         for mode in ((0, 1) if a.kernel != "pack" else (0,)):
             t_m = timed(lambda: update(sb, mode))
             res = {"kernel": a.kernel, "carveout": os.environ.get("HOD_CARVEOUT", "1"), "grid_cap": grid,
+                   "green_sms": a.green,
                    "adamw": "fast" if mode else "exact", "numel": n, "t_gemm": round(t_g, 3),
                    "t_mem": round(t_m, 3), "mem_GBps": round(nbytes / t_m / 1e6, 1)}
             for order in ("gemm_first", "mem_first"):
