@@ -63,11 +63,12 @@ def test_emulated_ranks_non_power_of_two(d):
     assert out["ok"]
 
 
-@pytest.mark.parametrize("d,clip", [(2, 0.0), (4, 0.02), (8, 0.0)])
-def test_emulated_ranks_tma_span_kernel(d, clip):
+@pytest.mark.parametrize("d,clip,flow", [(2, 0.0, "step"), (4, 0.02, "step"), (8, 0.0, "step"),
+                                         (4, 0.02, "hooks")])
+def test_emulated_ranks_tma_span_kernel(d, clip, flow):
     """The TMA-fed span kernel (HOD_SPAN_TMA=2: also under the emulation's
     grid cap) through the concurrent protocol, checked like the default."""
-    out = run_worker("--d", d, "--clip", clip, "--flow", "step", "--steps", 3, extra_env={"HOD_SPAN_TMA": "2"})
+    out = run_worker("--d", d, "--clip", clip, "--flow", flow, "--steps", 3, extra_env={"HOD_SPAN_TMA": "2"})
     assert out["ok"] and out["buckets"] > 3
 
 
